@@ -1,0 +1,197 @@
+/*
+ * dp.h — C-ABI of libdp.so: B200-native decentralized Wiener-filter (WF)
+ * precoding, the data-parallel hot path of arXiv 1804.10987
+ * ("Feedforward Architectures for Decentralized Precoding in Massive MU-MIMO
+ * Systems", Li, Jeon, Cavallaro, Studer).
+ *
+ * Citations: P:L = PAPER.md line L (LaTeX source); equation numbers follow
+ * the paper's LaTeX numbering.
+ *
+ * The calls follow the paper's problem statement
+ *     x   = P  (s, H,   N0, rho^2)       (P:87-91,  centralized)
+ *     x_c = P_c(s, H_c, N0, rho^2)       (Eq. 8, per cluster c)
+ * evaluated for every OFDM subcarrier w and every OFDM symbol k of a frame
+ * (N_sc independent narrowband systems, channel constant over K).
+ *
+ * Method (both precoders, per subcarrier):
+ *   PD-WF (Sec. III-B):  G_c = H_c H_c^H ; G = sum_c G_c ;
+ *       kappa = U N0/rho^2 (Eq. 5) ; A = G + kappa I_U ; Cholesky A = L L^H ;
+ *       A^{-1} by forward/back substitution ;
+ *       beta = sqrt(Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)) (Lemma 1, Eq. 6) ;
+ *       z_k = A^{-1} s_k / beta ; x_{c,k} = H_c^H z_k.
+ *   FD-WF (Sec. III-C):  per cluster, the same chain on H_c alone
+ *       with rho_c^2 = rho^2/C and kappa_c = tau U N0/rho_c^2 (Eq. 9).
+ *
+ * ---------------------------------------------------------------- layouts
+ * dp_c32 is an interleaved complex float (== cuComplex == torch.complex64).
+ * Antennas are numbered b = 0..B-1; cluster c owns antennas [c*S, (c+1)*S),
+ * S = B/C (equal split).  Rank r of `world` owns clusters
+ * [r*C/world, (r+1)*C/world), i.e. the contiguous antenna block
+ * [r*B/world, (r+1)*B/world) — "one GPU per cluster" with the
+ * cluster count C decoupled from the GPU count.
+ *   H_local  [n_sc][B/world][U]   H_local[w][b][u] = H^paper_{u, b0+b} of subcarrier w
+ *                                 (transpose of the paper's U x B, NOT conjugated)
+ *   s        [n_sc][K][U]         transmit symbols s_k of subcarrier w
+ *   x_local  [n_sc][K][B/world]   precoded x_k restricted to this rank's antennas
+ * Stacking the ranks' x_local along the last axis gives x[n_sc][K][B].
+ *
+ * ---------------------------------------------------------------- ownership
+ * Pointers may be DEVICE pointers (the fast path; the caller owns them, the
+ * call is asynchronous on `stream`) or HOST pointers (pinned or pageable; the
+ * library stages them through context-owned device buffers with H2D / D2H
+ * copies on `stream` and the call returns after the D2H copy completed).
+ * All of H_local, s, x_local must be of the same kind.  `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).
+ * The context owns every workspace (sized at dp_init; precode calls perform
+ * no allocation on the device-pointer path and are CUDA-graph capturable when
+ * world == 1) and, for world > 1, its own NCCL communicator.
+ * A context is not thread-safe; distinct contexts are independent.
+ *
+ * ---------------------------------------------------------------- errors
+ * Every call returns a dp_status code; dp_last_error() gives a thread-local
+ * message for the last failing call.  Numerical failures (A not Hermitian
+ * positive definite: Cholesky pivot <= 0 or non-finite, or beta radicand
+ * <= 0 — e.g. N0 = 0 with a rank-deficient H_c, or non-finite input) are
+ * detected on the device per (subcarrier, cluster); the affected outputs
+ * are set to zero and counted.  They are reported by dp_status(), or
+ * returned directly as DP_ERR_NUMERIC by the precode call when DP_FLAG_SYNC
+ * is set (the call then synchronizes `stream`).
+ */
+#ifndef DP_H_
+#define DP_H_
+
+#if defined(DP_BUILD) && defined(__GNUC__)
+#define DP_API __attribute__((visibility("default")))
+#else
+#define DP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define DP_OK              0
+#define DP_ERR_NUMERIC     1   /* A not HPD / beta undefined on >= 1 (subcarrier, cluster)      */
+#define DP_ERR_INVALID     2   /* bad argument: NULL pointer, dims, N0 < 0, rho2 <= 0, ...      */
+#define DP_ERR_CUDA        3   /* CUDA runtime error (message in dp_last_error)                 */
+#define DP_ERR_NCCL        4   /* NCCL error                                                    */
+#define DP_ERR_UNSUPPORTED 5   /* e.g. B/C < U (FD small-cluster branch), U > 32         */
+
+/* dp_config.flags */
+#define DP_FLAG_SYNC        1  /* synchronize at the end of each precode call; return numeric errors */
+#define DP_FLAG_UNFUSED     2  /* run the three-kernel path (a) Gram -> (b) solve+whiten -> (c) precode
+                                  even where the single-pass fused kernel applies                      */
+#define DP_FLAG_PROFILE     4  /* bracket every kernel launch with CUDA events (dp_profile_read)        */
+#define DP_FLAG_FORCE_COMM  8  /* world == 1: still issue the NCCL collectives (tests the comm path);
+                                  requires nccl_id                                                     */
+
+/* dp_config.pd_topology */
+#define DP_PD_ALLREDUCE     0  /* allreduce packed G; every rank solves redundantly (default)          */
+#define DP_PD_REDUCE_BCAST  1  /* paper's design: reduce G to rank 0, rank 0 solves
+                                  and whitens, broadcast z                                             */
+
+typedef struct { float re, im; } dp_c32;
+typedef struct dp_ctx dp_ctx;                       /* opaque */
+
+typedef struct {
+    int n_sc;            /* subcarriers per frame, > 0                                  */
+    int B;               /* BS antennas (all ranks), > 0                                        */
+    int U;               /* UEs, 1 <= U <= 32                                                   */
+    int K;               /* OFDM symbols per frame sharing one channel, 1..64           */
+    int C;               /* antenna clusters, B % C == 0, C % world == 0, B/C >= U              */
+    int rank, world;     /* this process's rank and the number of GPUs (one process per GPU)    */
+    int device;          /* CUDA device ordinal of this rank                                    */
+    const void *nccl_id; /* 128-byte ncclUniqueId from dp_get_unique_id on rank 0, identical on
+                            all ranks; NULL iff world == 1 (without DP_FLAG_FORCE_COMM)         */
+    double Es;           /* average symbol energy of the constellation (reading R1), > 0 */
+    double tau;          /* FD regularisation scale tau_c (Eq. 9; P:241 default 0.125), >= 0    */
+    int pd_topology;     /* DP_PD_ALLREDUCE or DP_PD_REDUCE_BCAST                               */
+    int s_on_all_ranks;  /* 1: s is valid on every rank; 0: s is read on rank 0 only and
+                            broadcast by the library ("s is the only signal that must be
+                            broadcast")                                    */
+    int flags;           /* DP_FLAG_*                                                           */
+} dp_config;
+
+/* scalar outputs readable after a precode call (dp_read_scalars `which`) */
+#define DP_SCALAR_BETA   0  /* PD: beta^WF[n_sc] (Lemma 1).  FD: this rank's beta_c[n_sc][C/world] */
+#define DP_SCALAR_RX     1  /* joint UE receive scale per subcarrier [n_sc]: PD beta^WF;
+                               FD 1 / sum_c (1/beta_c) over ALL clusters (reading R9)              */
+#define DP_SCALAR_POWER  2  /* sum_k ||x_k||^2 over ALL B antennas, per subcarrier [n_sc]
+                               (check of the power constraint, Eq. 2)                     */
+
+/* kernels reported by dp_profile_read (index into its arrays) */
+#define DP_KERNEL_FUSED_FD      0   /* single pass: Gram+solve+whiten+precode, one warp-group per cluster */
+#define DP_KERNEL_FUSED_PD      1   /* single pass PD (world == 1): Gram over all antennas ... precode    */
+#define DP_KERNEL_GRAM          2   /* (a) batched Gram, packed Hermitian output                          */
+#define DP_KERNEL_SOLVE         3   /* (b) regularise + Cholesky + substitution + beta + whiten z         */
+#define DP_KERNEL_PRECODE       4   /* (c) x_c = H_c^H z + power partials                                 */
+#define DP_KERNEL_SOLVE_PRECODE 5   /* (b)+(c) in one pass over H_local (PD, world > 1, allreduce)        */
+#define DP_KERNEL_FINISH        6   /* per-subcarrier scalar combination                                  */
+#define DP_NUM_KERNELS          7
+
+/* Fill `out128` with a fresh ncclUniqueId (call on rank 0 only, then share the
+ * 128 bytes with every rank, e.g. through torch.distributed). */
+DP_API int dp_get_unique_id(void *out128);
+
+/* Validate `cfg`, select `cfg->device`, allocate all workspace, and (world > 1)
+ * create the NCCL communicator (collective: every rank must call it).
+ * On success *out is a new context; on failure *out is NULL. */
+DP_API int dp_init(const dp_config *cfg, dp_ctx **out);
+
+/* PD-WF frame (Sec. III-B): x_local = H_local^H A^{-1} s / beta^WF for every
+ * subcarrier and symbol, with A = sum over ALL clusters (all ranks) of
+ * G_c + kappa I, kappa = U N0 / rho2.  Collective when world > 1.
+ * N0 >= 0 (noise variance per complex entry), rho2 > 0 (power budget, Eq. 2). */
+DP_API int dp_precode_pd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
+                  double N0, double rho2, dp_c32 *x_local, void *stream);
+
+/* FD-WF frame (Sec. III-C): for every local cluster c,
+ * x_c = H_c^H (H_c H_c^H + kappa_c I)^{-1} s / beta_c with rho_c^2 = rho2 / C,
+ * kappa_c = tau U N0 / rho_c^2.  Only s (and 2 n_sc scalars) cross ranks.
+ * Returns DP_ERR_UNSUPPORTED if B/C < U (branch B_c < U of P:230). */
+DP_API int dp_precode_fd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
+                  double N0, double rho2, dp_c32 *x_local, void *stream);
+
+/* Copy scalar output `which` (DP_SCALAR_*) of the last precode call into
+ * `dst` (device or host float array of the documented length), ordered on
+ * `stream`; a host `dst` is complete when the call returns. */
+DP_API int dp_read_scalars(dp_ctx *ctx, int which, float *dst, void *stream);
+
+/* Synchronize the context's work and report the number of (subcarrier,
+ * cluster) problems whose regularised Gram was not HPD since the last call
+ * (then reset it).  Returns DP_ERR_NUMERIC if that number is > 0. */
+DP_API int dp_status(dp_ctx *ctx, int *n_bad);
+
+/* Kernel-level profile (requires DP_FLAG_PROFILE): per DP_KERNEL_* the summed
+ * device milliseconds and launch counts since the last reset.  Synchronizes. */
+DP_API int dp_profile_read(dp_ctx *ctx, double *ms /*[DP_NUM_KERNELS]*/,
+                    long long *launches /*[DP_NUM_KERNELS]*/, int reset);
+
+/* Total kernels launched by this context since dp_init (all kinds). */
+DP_API long long dp_launch_count(dp_ctx *ctx);
+
+/* Destroy the communicator and free all workspace.  Does not touch caller
+ * buffers or streams.  NULL is accepted. */
+DP_API int dp_finalize(dp_ctx *ctx);
+
+/* Thread-local message describing the last error ("" if none). */
+DP_API const char *dp_last_error(void);
+
+/* --------------------------------------------------------------------------
+ * Test-only step exports (per-step parity).  Device pointers.
+ * dp_debug_gram:  G_packed[n_sc][groups][U(U+1)/2] = upper triangle (u <= v,
+ *   row-major) of sum_{b in group} h_b h_b^H, groups = C/world clusters
+ *   (per_cluster = 1) or 1 (all local antennas).
+ * dp_debug_solve: from G_packed [n_sc][groups][U(U+1)/2] and s: beta[n_sc][groups]
+ *   and z[n_sc][groups][K][U] = (G + kappa I)^{-1} s_k / beta, with
+ *   beta = sqrt(Es/rho_x2 (tr A^{-1} - kappa ||A^{-1}||_F^2)).
+ * -------------------------------------------------------------------------- */
+DP_API int dp_debug_gram(dp_ctx *ctx, const dp_c32 *H_local, int per_cluster, dp_c32 *G_packed, void *stream);
+DP_API int dp_debug_solve(dp_ctx *ctx, const dp_c32 *G_packed, int groups, const dp_c32 *s,
+                   double kappa, double rho_x2, float *beta, dp_c32 *z, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DP_H_ */

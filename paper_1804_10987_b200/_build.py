@@ -1,0 +1,76 @@
+"""Build libdp.so (CUDA, sm_100a) in-tree with nvcc.
+
+    python -m paper_1804_10987_b200._build [--force] [--verbose]
+
+The shared library links NCCL from the torch-bundled `nvidia.nccl` wheel
+(rpath set to its lib/ directory) and the static CUDA runtime.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libdp.so")
+SOURCES = [os.path.join(CSRC, "dp_api.cu")]
+DEPS = SOURCES + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "dp.h")]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    cands = []
+    try:
+        import nvidia.nccl as nn  # torch-bundled NCCL 2.28
+
+        base = list(nn.__path__)[0]
+        cands.append(base)
+    except Exception:
+        pass
+    cands += glob.glob("/opt/prime-rl/.venv/lib/python3*/site-packages/nvidia/nccl")
+    for b in cands:
+        inc, lib = os.path.join(b, "include"), os.path.join(b, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and glob.glob(os.path.join(lib, "libnccl.so*")):
+            return inc, lib
+    raise RuntimeError("NCCL headers/library not found (expected the nvidia-nccl wheel)")
+
+
+def nvcc():
+    for p in ("/usr/local/cuda/bin/nvcc", "nvcc"):
+        if os.path.sep not in p or os.path.exists(p):
+            return p
+    return "nvcc"
+
+
+def stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return LIB
+    inc, lib = nccl_dirs()
+    libname = os.path.basename(sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0])
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+           "-Xcompiler", "-fvisibility=hidden", "-DDP_BUILD",
+           "-I", INCLUDE, "-I", CSRC, "-I", inc,
+           *SOURCES, "-o", LIB + ".tmp",
+           "-L", lib, f"-l:{libname}", "-Xlinker", f"-rpath,{lib}"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)

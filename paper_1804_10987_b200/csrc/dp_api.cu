@@ -1,0 +1,706 @@
+// dp_api.cu — C-ABI of libdp.so (see include/dp.h for the contract).
+//
+// Host side of the B200-native decentralized WF precoders (arXiv 1804.10987):
+// argument validation, workspace ownership, kernel dispatch over U, NCCL
+// exchange steps (PD: Gram reduction P:280-281 and, in the paper's topology,
+// z broadcast P:296; FD: s broadcast P:255/P:299 and a 2*n_sc scalar
+// allreduce), host-pointer staging and kernel-level profiling.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dp.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(DP_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,   \
+                                       cudaGetErrorString(e_));                                   \
+  } while (0)
+#define NK(call)                                                                                  \
+  do {                                                                                            \
+    ncclResult_t r_ = (call);                                                                     \
+    if (r_ != ncclSuccess) return fail(DP_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,   \
+                                       ncclGetErrorString(r_));                                   \
+  } while (0)
+#define RET(call)                 \
+  do {                            \
+    int rc_ = (call);             \
+    if (rc_ != DP_OK) return rc_; \
+  } while (0)
+
+struct ProfRec {
+  int kid;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct dp_ctx {
+  dp_config cfg;
+  int Bl = 0;        // antennas on this rank
+  int Cl = 0;        // clusters on this rank
+  int S = 0;         // cluster size B / C
+  int pd_chunk = 0;  // rows per SG chunk in the per-subcarrier PD kernels
+  int pd_nchunks = 0;
+  int pd_nw = 0;     // warps per CTA of the per-subcarrier PD kernels
+  int fd_nw = 0;     // warps per CTA of the FD fused kernel
+  int fdu_nw = 0;    // warps of the FD unfused per-subcarrier kernels (chunk = cluster)
+  bool comm_on = false;
+  ncclComm_t comm = nullptr;
+  // device workspace
+  float2 *s_buf = nullptr;   // broadcast landing buffer for s
+  float2 *G = nullptr;       // packed Grams
+  float2 *z = nullptr;       // whitened symbols (unfused / T1)
+  float *beta = nullptr;     // per problem beta
+  float *pw = nullptr;       // power partials
+  float *fin = nullptr;      // [n_sc][2] per-subcarrier scalars
+  int *bad = nullptr;        // non-HPD counter
+  size_t pw_len = 0;
+  // host staging (host-pointer calls)
+  float2 *h_dev = nullptr, *s_dev = nullptr, *x_dev = nullptr;
+  // last call
+  int last_mode = -1;        // 0 pd, 1 fd
+  // profiling
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[DP_NUM_KERNELS] = {0};
+  long long prof_n[DP_NUM_KERNELS] = {0};
+  long long launches = 0;
+};
+
+namespace {
+
+int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+int kc_of(int K) { return (K % 7 == 0) ? 7 : 8; }
+
+template <int KC>
+int zs_of(int K) { return dpk::ZL<KC>::zs(K); }
+int zs_rt(int K) { return kc_of(K) == 7 ? zs_of<7>(K) : zs_of<8>(K); }
+
+// ---------------------------------------------------------------- smem sizes (bytes)
+size_t smem_fd_fused(int U, int S, int K, int nw) {
+  const int PPW = 32 / U;
+  const int scr = std::max(U + U * (U + 2), U * zs_rt(K));
+  return (size_t)nw * PPW * (S * U + scr) * sizeof(float2);
+}
+size_t smem_sc(int U, int Bl, int K, int nw, int zgroups) {
+  const int PPW = 32 / U;
+  size_t e = (size_t)Bl * U + (size_t)(nw / 2) * U * (U + 2) + (size_t)PPW * (U + U * (U + 2)) +
+             (size_t)zgroups * U * zs_rt(K);
+  return e * sizeof(float2);
+}
+size_t smem_solve(int U) { return (size_t)4 * (32 / U) * (U + U * (U + 2)) * sizeof(float2); }
+
+// ---------------------------------------------------------------- profiling helpers
+cudaEvent_t take_event(dp_ctx *c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct LaunchScope {
+  dp_ctx *c;
+  int kid;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  LaunchScope(dp_ctx *c_, int kid_, cudaStream_t st_) : c(c_), kid(kid_), st(st_) {
+    c->launches++;
+    if (c->cfg.flags & DP_FLAG_PROFILE) {
+      a = take_event(c);
+      b = take_event(c);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~LaunchScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      c->prof.push_back({kid, a, b});
+    }
+  }
+};
+
+int drain_profile(dp_ctx *c) {
+  for (auto &r : c->prof) {
+    CK(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    c->prof_ms[r.kid] += ms;
+    c->prof_n[r.kid] += 1;
+    c->ev_pool.push_back(r.a);
+    c->ev_pool.push_back(r.b);
+  }
+  c->prof.clear();
+  return DP_OK;
+}
+
+// ---------------------------------------------------------------- kernel launchers
+using dpk::Args;
+
+template <int U, int KC>
+int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
+  const int nw = c->fd_nw;
+  const int nsg = nw * (32 / U);
+  const int nprob = a.n_sc * a.nchunks;
+  const size_t sm = smem_fd_fused(U, a.S, a.K, nw);
+  auto kern = dpk::fd_fused_kernel<U, KC>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
+  kern<<<(nprob + nsg - 1) / nsg, nw * 32, sm, st>>>(a);
+  CK(cudaGetLastError());
+  return DP_OK;
+}
+
+template <int U, int KC, int MODE, bool PER_CHUNK>
+int launch_sc(dp_ctx *c, const Args &a, int nw, int kid, cudaStream_t st) {
+  const size_t sm = smem_sc(U, a.Bl, a.K, nw, MODE == dpk::MODE_PRECODE ? a.zgroups : 1);
+  auto kern = dpk::sc_kernel<U, KC, MODE, PER_CHUNK>;
+  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "per-subcarrier tile needs %zu B of shared memory", sm);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  LaunchScope ls(c, kid, st);
+  kern<<<a.n_sc, nw * 32, sm, st>>>(a);
+  CK(cudaGetLastError());
+  return DP_OK;
+}
+
+template <int U>
+int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
+  const int per = 4 * (32 / U);
+  const int nprob = a.n_sc * a.groups;
+  const size_t sm = smem_solve(U);
+  auto kern = dpk::solve_kernel<U>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  LaunchScope ls(c, DP_KERNEL_SOLVE, st);
+  kern<<<(nprob + per - 1) / per, 128, sm, st>>>(a);
+  CK(cudaGetLastError());
+  return DP_OK;
+}
+
+int launch_finish(dp_ctx *c, const float *beta, int nbeta, const float *pw, int npw, int fd,
+                  cudaStream_t st) {
+  LaunchScope ls(c, DP_KERNEL_FINISH, st);
+  dpk::finish_kernel<<<(c->cfg.n_sc + 127) / 128, 128, 0, st>>>(beta, nbeta, pw, npw, c->cfg.n_sc, fd, c->fin);
+  CK(cudaGetLastError());
+  return DP_OK;
+}
+
+// ---------------------------------------------------------------- U / KC dispatch
+template <template <int, int> class F, typename... T>
+int dispatch(int U, int K, T... args) {
+  const bool k7 = kc_of(K) == 7;
+  switch (U) {
+    case 4: return k7 ? F<4, 7>::run(args...) : F<4, 8>::run(args...);
+    case 8: return k7 ? F<8, 7>::run(args...) : F<8, 8>::run(args...);
+    case 16: return k7 ? F<16, 7>::run(args...) : F<16, 8>::run(args...);
+    case 32: return k7 ? F<32, 7>::run(args...) : F<32, 8>::run(args...);
+  }
+  return fail(DP_ERR_UNSUPPORTED, "U=%d: kernels are instantiated for U in {4, 8, 16, 32}", U);
+}
+
+template <int U, int KC> struct FdFused {
+  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_fd_fused<U, KC>(c, a, st); }
+};
+template <int U, int KC> struct PdFused {
+  static int run(dp_ctx *c, Args a, cudaStream_t st) {
+    return launch_sc<U, KC, dpk::MODE_PD_FUSED, false>(c, a, c->pd_nw, DP_KERNEL_FUSED_PD, st);
+  }
+};
+template <int U, int KC> struct GramSum {
+  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) {
+    return launch_sc<U, 8, dpk::MODE_GRAM, false>(c, a, nw, DP_KERNEL_GRAM, st);
+  }
+};
+template <int U, int KC> struct GramPer {
+  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) {
+    return launch_sc<U, 8, dpk::MODE_GRAM, true>(c, a, nw, DP_KERNEL_GRAM, st);
+  }
+};
+template <int U, int KC> struct SolvePrecode {
+  static int run(dp_ctx *c, Args a, cudaStream_t st) {
+    return launch_sc<U, KC, dpk::MODE_SOLVE_PRECODE, false>(c, a, c->pd_nw, DP_KERNEL_SOLVE_PRECODE, st);
+  }
+};
+template <int U, int KC> struct Precode {
+  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) {
+    return launch_sc<U, KC, dpk::MODE_PRECODE, false>(c, a, nw, DP_KERNEL_PRECODE, st);
+  }
+};
+template <int U, int KC> struct Solve {
+  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_solve<U>(c, a, st); }
+};
+
+// ---------------------------------------------------------------- helpers
+int alloc(void **p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  CK(cudaMalloc(p, bytes));
+  CK(cudaMemset(*p, 0, bytes));
+  return DP_OK;
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int validate_call(dp_ctx *c, const void *H, const void *s, double N0, double rho2, void *x) {
+  if (!c) return fail(DP_ERR_INVALID, "ctx is NULL");
+  if (!H || !x) return fail(DP_ERR_INVALID, "H_local and x_local must be non-NULL");
+  const bool need_s = c->cfg.s_on_all_ranks || c->cfg.rank == 0;
+  if (need_s && !s) return fail(DP_ERR_INVALID, "s must be non-NULL on this rank");
+  if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0 (got %g)", N0);
+  if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0 (got %g)", rho2);
+  return DP_OK;
+}
+
+Args base_args(dp_ctx *c) {
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.n_sc = c->cfg.n_sc;
+  a.Bl = c->Bl;
+  a.K = c->cfg.K;
+  a.beta = c->beta;
+  a.pw = c->pw;
+  a.bad = c->bad;
+  return a;
+}
+
+// Stage host pointers into device buffers (H2D on st).  Returns device views.
+int stage_in(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, dp_c32 *x, cudaStream_t st, bool *host,
+             const float2 **Hd, const float2 **sd, float2 **xd) {
+  const bool hdev = is_device_ptr(H), xdev = is_device_ptr(x);
+  const bool sdev = s ? is_device_ptr(s) : hdev;
+  if (hdev != xdev || hdev != sdev)
+    return fail(DP_ERR_INVALID, "H_local, s and x_local must all be device pointers or all host pointers");
+  *host = !hdev;
+  const size_t nH = (size_t)c->cfg.n_sc * c->Bl * c->cfg.U, nS = (size_t)c->cfg.n_sc * c->cfg.K * c->cfg.U,
+               nX = (size_t)c->cfg.n_sc * c->cfg.K * c->Bl;
+  if (hdev) {
+    *Hd = reinterpret_cast<const float2 *>(H);
+    *sd = reinterpret_cast<const float2 *>(s);
+    *xd = reinterpret_cast<float2 *>(x);
+    return DP_OK;
+  }
+  if (!c->h_dev) {
+    RET(alloc((void **)&c->h_dev, nH * 8));
+    RET(alloc((void **)&c->s_dev, nS * 8));
+    RET(alloc((void **)&c->x_dev, nX * 8));
+  }
+  CK(cudaMemcpyAsync(c->h_dev, H, nH * 8, cudaMemcpyHostToDevice, st));
+  if (s) CK(cudaMemcpyAsync(c->s_dev, s, nS * 8, cudaMemcpyHostToDevice, st));
+  *Hd = c->h_dev;
+  *sd = s ? c->s_dev : nullptr;
+  *xd = c->x_dev;
+  return DP_OK;
+}
+
+int stage_out(dp_ctx *c, bool host, dp_c32 *x, cudaStream_t st) {
+  if (!host) return DP_OK;
+  const size_t nX = (size_t)c->cfg.n_sc * c->cfg.K * c->Bl;
+  CK(cudaMemcpyAsync(x, c->x_dev, nX * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DP_OK;
+}
+
+// s broadcast from rank 0 ("the vector s is the only signal that must be broadcast")
+int distribute_s(dp_ctx *c, const float2 *s, cudaStream_t st, const float2 **s_use) {
+  if (!c->comm_on || c->cfg.s_on_all_ranks) {
+    *s_use = s;
+    return DP_OK;
+  }
+  const size_t n = (size_t)c->cfg.n_sc * c->cfg.K * c->cfg.U * 2;
+  if (c->cfg.rank == 0) {
+    NK(ncclBroadcast(s, (void *)s, n, ncclFloat, 0, c->comm, st));
+    *s_use = s;
+  } else {
+    NK(ncclBroadcast(nullptr, c->s_buf, n, ncclFloat, 0, c->comm, st));
+    *s_use = c->s_buf;
+  }
+  return DP_OK;
+}
+
+int finish_call(dp_ctx *c, bool host, dp_c32 *x, cudaStream_t st) {
+  RET(stage_out(c, host, x, st));
+  if (c->cfg.flags & DP_FLAG_SYNC) {
+    CK(cudaStreamSynchronize(st));
+    int nb = 0;
+    CK(cudaMemcpy(&nb, c->bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (nb > 0) {
+      CK(cudaMemset(c->bad, 0, sizeof(int)));
+      return fail(DP_ERR_NUMERIC, "%d (subcarrier, cluster) problems had a non-HPD regularised Gram", nb);
+    }
+  }
+  return DP_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char *dp_last_error(void) { return g_err.c_str(); }
+
+int dp_get_unique_id(void *out128) {
+  if (!out128) return fail(DP_ERR_INVALID, "out128 is NULL");
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out128, &id, sizeof(id));
+  return DP_OK;
+}
+
+int dp_init(const dp_config *cfg, dp_ctx **out) {
+  g_err.clear();
+  if (!out) return fail(DP_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(DP_ERR_INVALID, "cfg is NULL");
+  const dp_config &k = *cfg;
+  if (k.n_sc <= 0 || k.B <= 0 || k.U <= 0 || k.K <= 0 || k.C <= 0)
+    return fail(DP_ERR_INVALID, "dims must be positive (n_sc=%d B=%d U=%d K=%d C=%d)", k.n_sc, k.B, k.U, k.K, k.C);
+  if (k.K > 64) return fail(DP_ERR_INVALID, "K=%d > 64", k.K);
+  if (k.world <= 0 || k.rank < 0 || k.rank >= k.world) return fail(DP_ERR_INVALID, "rank %d / world %d", k.rank, k.world);
+  if (k.B % k.C) return fail(DP_ERR_INVALID, "B=%d not divisible by C=%d (equal clusters, P:157)", k.B, k.C);
+  if (k.C % k.world) return fail(DP_ERR_INVALID, "C=%d not divisible by world=%d", k.C, k.world);
+  if (!(k.Es > 0.0) || !std::isfinite(k.Es)) return fail(DP_ERR_INVALID, "Es must be > 0");
+  if (!(k.tau >= 0.0) || !std::isfinite(k.tau)) return fail(DP_ERR_INVALID, "tau must be >= 0");
+  if (k.pd_topology != DP_PD_ALLREDUCE && k.pd_topology != DP_PD_REDUCE_BCAST)
+    return fail(DP_ERR_INVALID, "pd_topology %d", k.pd_topology);
+  if (k.U != 4 && k.U != 8 && k.U != 16 && k.U != 32)
+    return fail(DP_ERR_UNSUPPORTED, "U=%d: supported U are 4, 8, 16, 32", k.U);
+  const int S = k.B / k.C;
+  if (S < k.U) return fail(DP_ERR_UNSUPPORTED, "B/C=%d < U=%d (FD branch B_c < U, P:230, not implemented)", S, k.U);
+  const bool comm_on = k.world > 1 || (k.flags & DP_FLAG_FORCE_COMM);
+  if (comm_on && !k.nccl_id) return fail(DP_ERR_INVALID, "nccl_id is required when world > 1 or DP_FLAG_FORCE_COMM");
+
+  CK(cudaSetDevice(k.device));
+  dp_ctx *c = new dp_ctx();
+  c->cfg = k;
+  c->comm_on = comm_on;
+  c->Bl = k.B / k.world;
+  c->Cl = k.C / k.world;
+  c->S = S;
+  // per-subcarrier PD kernels: split clusters into chunks (>= U rows) until the
+  // CTA has >= 256 threads of SGs
+  int chunk = S;
+  while ((c->Bl / chunk) * k.U < 256 && chunk % 2 == 0 && chunk / 2 >= k.U) chunk /= 2;
+  c->pd_chunk = chunk;
+  c->pd_nchunks = c->Bl / chunk;
+  c->pd_nw = next_pow2((c->pd_nchunks * k.U + 31) / 32);
+  c->fdu_nw = next_pow2((c->Cl * k.U + 31) / 32);
+  // FD fused: 4 warps, fewer if smem would not fit
+  c->fd_nw = 4;
+  while (c->fd_nw > 1 && smem_fd_fused(k.U, S, k.K, c->fd_nw) > 100 * 1024) c->fd_nw >>= 1;
+  if (smem_fd_fused(k.U, S, k.K, c->fd_nw) > 227 * 1024) {
+    delete c;
+    return fail(DP_ERR_UNSUPPORTED, "cluster tile S=%d x U=%d does not fit in shared memory", S, k.U);
+  }
+  if (c->pd_nw > 8) {
+    delete c;
+    return fail(DP_ERR_UNSUPPORTED, "B/world=%d antennas per rank need %d warps per subcarrier (max 8)", c->Bl, c->pd_nw);
+  }
+  const int NP = dpk::npacked(k.U);
+  const size_t n_sc = k.n_sc;
+  const size_t groups = std::max(c->Cl, 1);
+  int rc = DP_OK;
+  auto A = [&](void **p, size_t b) {
+    if (rc == DP_OK) rc = alloc(p, b);
+  };
+  if (comm_on && !k.s_on_all_ranks) A((void **)&c->s_buf, n_sc * k.K * k.U * 8);
+  A((void **)&c->G, n_sc * groups * NP * 8);
+  A((void **)&c->z, n_sc * groups * k.K * k.U * 8);
+  A((void **)&c->beta, n_sc * groups * 4);
+  c->pw_len = n_sc * std::max<size_t>(std::max(c->pd_nchunks, c->Cl), 1);
+  A((void **)&c->pw, c->pw_len * 4);
+  A((void **)&c->fin, n_sc * 2 * 4);
+  A((void **)&c->bad, 4);
+  if (rc != DP_OK) {
+    std::string e = g_err;
+    dp_finalize(c);
+    g_err = e;
+    return rc;
+  }
+  if (comm_on) {
+    ncclUniqueId id;
+    memcpy(&id, k.nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, k.world, id, k.rank);
+    if (r != ncclSuccess) {
+      dp_finalize(c);
+      return fail(DP_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = c;
+  return DP_OK;
+}
+
+int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
+  g_err.clear();
+  RET(validate_call(c, H, s, N0, rho2, x));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->cfg.device));
+  const dp_config &k = c->cfg;
+  bool host;
+  const float2 *Hd, *sd;
+  float2 *xd;
+  RET(stage_in(c, H, s, x, st, &host, &Hd, &sd, &xd));
+  const float2 *s_use;
+  RET(distribute_s(c, sd, st, &s_use));
+  // FD parameters (Sec. III-C): rho_c^2 = rho^2/C, kappa_c = tau U N0 / rho_c^2 (Eq. 9)
+  const double rho_c2 = rho2 / k.C;
+  Args a = base_args(c);
+  a.H = Hd;
+  a.s = s_use;
+  a.x = xd;
+  a.S = c->S;
+  a.nchunks = c->Cl;
+  a.kappa = (float)(k.tau * k.U * N0 / rho_c2);
+  a.coef = (float)(k.Es / rho_c2);
+  if (k.flags & DP_FLAG_UNFUSED) {
+    // (a) per-cluster Grams -> (b) solve+whiten per cluster -> (c) precode
+    a.Gout = c->G;
+    RET(dispatch<GramPer>(k.U, k.K, c, a, c->fdu_nw, st));
+    a.G = c->G;
+    a.groups = c->Cl;
+    a.zout = c->z;
+    RET(dispatch<Solve>(k.U, k.K, c, a, st));
+    a.zin = c->z;
+    a.zgroups = c->Cl;
+    a.chunks_per_zgroup = 1;
+    RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
+  } else {
+    RET(dispatch<FdFused>(k.U, k.K, c, a, st));
+  }
+  RET(launch_finish(c, c->beta, c->Cl, c->pw, c->Cl, 1, st));
+  if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+  c->last_mode = 1;
+  return finish_call(c, host, x, st);
+}
+
+int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
+  g_err.clear();
+  RET(validate_call(c, H, s, N0, rho2, x));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->cfg.device));
+  const dp_config &k = c->cfg;
+  bool host;
+  const float2 *Hd, *sd;
+  float2 *xd;
+  RET(stage_in(c, H, s, x, st, &host, &Hd, &sd, &xd));
+  // PD parameters (Theorem 1, Eq. 5): kappa = U N0 / rho^2 ; beta via Lemma 1 with rho^2
+  Args a = base_args(c);
+  a.H = Hd;
+  a.x = xd;
+  a.S = c->pd_chunk;
+  a.nchunks = c->pd_nchunks;
+  a.kappa = (float)(k.U * N0 / rho2);
+  a.coef = (float)(k.Es / rho2);
+  a.groups = 1;
+  const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
+  const float2 *s_use = sd;
+  if (!topo_t1) RET(distribute_s(c, sd, st, &s_use));   // T2: overlaps nothing yet; only s crosses
+  a.s = s_use;
+  if (!c->comm_on) {
+    if (k.flags & DP_FLAG_UNFUSED) {
+      a.Gout = c->G;
+      RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
+      a.G = c->G;
+      a.zout = c->z;
+      RET(dispatch<Solve>(k.U, k.K, c, a, st));
+      a.zin = c->z;
+      a.zgroups = 1;
+      a.chunks_per_zgroup = c->pd_nchunks;
+      RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
+    } else {
+      RET(dispatch<PdFused>(k.U, k.K, c, a, st));
+    }
+  } else {
+    const size_t nG = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
+    // (a) local Gram: sum over this rank's clusters (the first adder-tree level)
+    a.Gout = c->G;
+    RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
+    a.G = c->G;
+    if (!topo_t1) {
+      // cross-rank adder tree G = sum_c G_c on every rank, then solve + precode in one pass
+      NK(ncclAllReduce(c->G, c->G, nG, ncclFloat, ncclSum, c->comm, st));
+      RET(dispatch<SolvePrecode>(k.U, k.K, c, a, st));
+    } else {
+      // paper topology: reduce to the master, master whitens, broadcast z
+      NK(ncclReduce(c->G, c->G, nG, ncclFloat, ncclSum, 0, c->comm, st));
+      if (k.rank == 0) {
+        a.zout = c->z;
+        RET(dispatch<Solve>(k.U, k.K, c, a, st));
+      }
+      NK(ncclGroupStart());
+      NK(ncclBroadcast(c->z, c->z, (size_t)k.n_sc * k.K * k.U * 2, ncclFloat, 0, c->comm, st));
+      NK(ncclBroadcast(c->beta, c->beta, (size_t)k.n_sc, ncclFloat, 0, c->comm, st));
+      NK(ncclGroupEnd());
+      a.zin = c->z;
+      a.zgroups = 1;
+      a.chunks_per_zgroup = c->pd_nchunks;
+      RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
+    }
+  }
+  // per-subcarrier scalars: 1/beta contributed once (rank 0), power summed over ranks
+  RET(launch_finish(c, c->beta, 1, c->pw, c->pd_nchunks, 0, st));
+  if (c->comm_on) {
+    if (k.rank != 0) {
+      // zero this rank's 1/beta contribution (stride-2 entries) before the sum
+      CK(cudaMemset2DAsync(c->fin, 2 * sizeof(float), 0, sizeof(float), k.n_sc, st));
+    }
+    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+  }
+  c->last_mode = 0;
+  return finish_call(c, host, x, st);
+}
+
+int dp_read_scalars(dp_ctx *c, int which, float *dst, void *stream) {
+  g_err.clear();
+  if (!c || !dst) return fail(DP_ERR_INVALID, "ctx/dst is NULL");
+  if (c->last_mode < 0) return fail(DP_ERR_INVALID, "no precode call yet");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->cfg.device));
+  const bool dev = is_device_ptr(dst);
+  const int n_sc = c->cfg.n_sc;
+  if (which == DP_SCALAR_BETA) {
+    const size_t n = (size_t)n_sc * (c->last_mode == 1 ? c->Cl : 1);
+    CK(cudaMemcpyAsync(dst, c->beta, n * 4, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  } else if (which == DP_SCALAR_RX || which == DP_SCALAR_POWER) {
+    float *d = dst;
+    float *tmp = nullptr;
+    if (!dev) {
+      CK(cudaMallocAsync((void **)&tmp, (size_t)n_sc * 4, st));
+      d = tmp;
+    }
+    dpk::read_scalars_kernel<<<(n_sc + 127) / 128, 128, 0, st>>>(c->fin, n_sc, which, d);
+    CK(cudaGetLastError());
+    if (!dev) {
+      CK(cudaMemcpyAsync(dst, tmp, (size_t)n_sc * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaFreeAsync(tmp, st));
+    }
+  } else {
+    return fail(DP_ERR_INVALID, "unknown scalar %d", which);
+  }
+  if (!dev) CK(cudaStreamSynchronize(st));
+  return DP_OK;
+}
+
+int dp_status(dp_ctx *c, int *n_bad) {
+  g_err.clear();
+  if (!c) return fail(DP_ERR_INVALID, "ctx is NULL");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaDeviceSynchronize());
+  if (c->comm) {
+    ncclResult_t async_err;
+    NK(ncclCommGetAsyncError(c->comm, &async_err));
+    if (async_err != ncclSuccess) return fail(DP_ERR_NCCL, "NCCL async error: %s", ncclGetErrorString(async_err));
+  }
+  int nb = 0;
+  CK(cudaMemcpy(&nb, c->bad, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(c->bad, 0, sizeof(int)));
+  if (n_bad) *n_bad = nb;
+  if (nb > 0) return fail(DP_ERR_NUMERIC, "%d (subcarrier, cluster) problems had a non-HPD regularised Gram", nb);
+  return DP_OK;
+}
+
+int dp_profile_read(dp_ctx *c, double *ms, long long *launches, int reset) {
+  g_err.clear();
+  if (!c) return fail(DP_ERR_INVALID, "ctx is NULL");
+  RET(drain_profile(c));
+  for (int i = 0; i < DP_NUM_KERNELS; ++i) {
+    if (ms) ms[i] = c->prof_ms[i];
+    if (launches) launches[i] = c->prof_n[i];
+    if (reset) {
+      c->prof_ms[i] = 0;
+      c->prof_n[i] = 0;
+    }
+  }
+  return DP_OK;
+}
+
+long long dp_launch_count(dp_ctx *c) { return c ? c->launches : 0; }
+
+int dp_finalize(dp_ctx *c) {
+  if (!c) return DP_OK;
+  cudaSetDevice(c->cfg.device);
+  cudaDeviceSynchronize();
+  drain_profile(c);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  delete c;
+  return DP_OK;
+}
+
+// ---------------------------------------------------------------- test-only step exports
+int dp_debug_gram(dp_ctx *c, const dp_c32 *H, int per_cluster, dp_c32 *G, void *stream) {
+  g_err.clear();
+  if (!c || !H || !G) return fail(DP_ERR_INVALID, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  Args a = base_args(c);
+  a.H = reinterpret_cast<const float2 *>(H);
+  a.Gout = reinterpret_cast<float2 *>(G);
+  if (per_cluster) {
+    a.S = c->S;
+    a.nchunks = c->Cl;
+    RET(dispatch<GramPer>(c->cfg.U, c->cfg.K, c, a, c->fdu_nw, st));
+  } else {
+    a.S = c->pd_chunk;
+    a.nchunks = c->pd_nchunks;
+    RET(dispatch<GramSum>(c->cfg.U, c->cfg.K, c, a, c->pd_nw, st));
+  }
+  return DP_OK;
+}
+
+int dp_debug_solve(dp_ctx *c, const dp_c32 *G, int groups, const dp_c32 *s, double kappa, double rho_x2,
+                   float *beta, dp_c32 *z, void *stream) {
+  g_err.clear();
+  if (!c || !G || !s || !beta || !z || groups <= 0) return fail(DP_ERR_INVALID, "bad argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  Args a = base_args(c);
+  a.G = reinterpret_cast<const float2 *>(G);
+  a.s = reinterpret_cast<const float2 *>(s);
+  a.groups = groups;
+  a.zout = reinterpret_cast<float2 *>(z);
+  a.beta = beta;
+  a.kappa = (float)kappa;
+  a.coef = (float)(c->cfg.Es / rho_x2);
+  RET(dispatch<Solve>(c->cfg.U, c->cfg.K, c, a, st));
+  return DP_OK;
+}
+
+}  // extern "C"
