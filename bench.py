@@ -1,0 +1,426 @@
+"""bench.py — precoded Gbit/s and frame latency (device-timed) of PD-WF and FD-WF.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[3]): B=256 antennas, U=32 UEs,
+C=8 clusters (S=32), N_sc=1200 subcarriers, K=14 OFDM symbols, 64-QAM, SNR
+10 dB, tau=0.125.  A STEP is one pass of the whole hot path over one frame:
+one PD-WF frame followed by one FD-WF frame, so
+bits/step = 2 * N_sc * K * U * log2(M) for the whole job.  Scaling is STRONG
+(the frame is fixed; clusters are sharded over the N GPUs, C/N per GPU).
+
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
+CUDA events on the launching stream, max over ranks.  Inputs rotate over R
+resident input sets whose total size exceeds 2x L2 (126 MB), so every step
+reads H from HBM.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "precoded Gbit/s and frame latency (device-timed) for PD/FD WF at 1/2/4/8 B200"
+L2_BYTES = 126 * 1024 * 1024
+SEED = 180410987
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="both", choices=["both", "pd", "fd"])
+    ap.add_argument("--unfused", action="store_true", help="three-kernel path (a)(b)(c)")
+    ap.add_argument("--pd-topology", default="allreduce", choices=["allreduce", "reduce_bcast"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time for cpu_baseline")
+    ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no JSON extras)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- algorithmic work
+def flops_problem(U: int, nb: int, K: int) -> dict:
+    """Algorithmic real flops of one WF problem (one subcarrier x one cluster for FD, one
+    subcarrier over nb antennas for PD); complex MAC = 8 flops.
+    Gram: Hermitian half U(U+1)/2 entries x nb ; Cholesky U^3/6 ; L^-1 U^3/6 ; A^-1 = W0^H W0 U^3/6 ;
+    whiten K U^2 ; precode K nb U."""
+    cmac = {
+        "gram": nb * U * (U + 1) / 2,
+        "solve": U ** 3 / 2,
+        "whiten": K * U * U,
+        "precode": K * nb * U,
+    }
+    return {k: 8.0 * v for k, v in cmac.items()}
+
+
+def bytes_frame(cfg, Bl: int) -> dict:
+    """Algorithmic HBM bytes per frame per GPU: H read once, s read once, x written once."""
+    return {"H": cfg.n_sc * Bl * cfg.U * 8, "s": cfg.n_sc * cfg.K * cfg.U * 8, "x": cfg.n_sc * cfg.K * Bl * 8}
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return self
+
+        def rd():
+            for line in self.proc.stdout:
+                self.rows.append([c.strip() for c in line.split(",")])
+
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- oracle CPU baseline
+def cpu_baseline(cfg, target_s: float):
+    """The fp64 oracle (oracle/, as it stands) on a bounded sample of the same workload:
+    the first n subcarriers of one frame, PD + FD, on all host cores (OpenMP)."""
+    import numpy as np
+
+    import oracle
+    from paper_1804_10987_b200 import synth
+
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+
+    def run(n):
+        f = synth.make_frame(cfg.cfg_id, n, cfg.B, cfg.U, cfg.K, cfg.M, frame=77)
+        t = time.perf_counter()
+        oracle.pd(f.H, f.s, cfg.C, N0)
+        oracle.fd(f.H, f.s, cfg.C, N0, tau=cfg.tau)
+        return time.perf_counter() - t
+
+    cores = oracle.num_threads()
+    n0 = max(cores, 8)
+    t0 = run(n0)
+    n = int(min(cfg.n_sc * 4, max(n0, n0 * target_s / max(t0, 1e-3))))
+    t = run(n)
+    bits = 2 * n * cfg.K * cfg.U * (cfg.M.bit_length() - 1)
+    return {"value": bits / t / 1e9, "unit": "Gbit/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} subcarriers of {cfg.name} (PD + FD, fp64 C oracle, OpenMP over subcarriers), "
+                      f"{t:.2f} s", "seconds": t, "subcarriers": n}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    import oracle  # noqa: F401
+    per_step = max(1, int(args.cpu_seconds / max(args.steps + args.warmup, 1)))
+    base = cpu_baseline(cfg, target_s=max(2.0, min(args.cpu_seconds, 20.0) / 2))
+    # steps: each step is a bounded sample (base['subcarriers'] subcarriers); time per step
+    import numpy as np  # noqa: F401
+    from paper_1804_10987_b200 import synth
+    import oracle as orc
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    n = max(8, base["subcarriers"] // 4)
+    f = synth.make_frame(cfg.cfg_id, n, cfg.B, cfg.U, cfg.K, cfg.M, frame=78)
+    for _ in range(args.warmup):
+        orc.pd(f.H[:8], f.s[:8], cfg.C, N0)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        orc.pd(f.H, f.s, cfg.C, N0)
+        orc.fd(f.H, f.s, cfg.C, N0, tau=cfg.tau)
+    el = time.perf_counter() - t
+    bits = 2 * n * cfg.K * cfg.U * (cfg.M.bit_length() - 1) * args.steps
+    v = bits / el / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gbit/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
+            "data": "synthetic", "config": {"workload": cfg.name, "sample_subcarriers_per_step": n},
+            "cpu_baseline": {"value": v, "unit": "Gbit/s", "cores": base["cores"], "kind": "oracle",
+                             "sample": f"{n} of {cfg.n_sc} subcarriers per step, PD + FD"},
+            "e2e": {"value": v, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    _ = per_step
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+def main():
+    args = parse()
+    from paper_1804_10987_b200 import CONFIGS
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print(f"--gpus {args.gpus} != WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1804_10987_b200 import _lib as L
+    from paper_1804_10987_b200 import synth
+    from paper_1804_10987_b200.api import Precoder
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if cfg.C % world:
+        raise SystemExit(f"C={cfg.C} not divisible by {world} GPUs")
+    Bl = cfg.B // world
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+
+    # NCCL id for the library's own communicator
+    uid = None
+    if world > 1:
+        obj = [L.dp_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    flags = L.DP_FLAG_PROFILE | (L.DP_FLAG_UNFUSED if args.unfused else 0)
+    pre = Precoder(cfg.n_sc, cfg.B, cfg.U, cfg.K, cfg.C, rank=rank, world=world, device=local, tau=cfg.tau,
+                   pd_topology=args.pd_topology, s_on_all_ranks=(world == 1), flags=flags, nccl_id=uid)
+
+    # ---------------- resident rotating input sets (> 2x L2 in total)
+    bf = bytes_frame(cfg, Bl)
+    per_set = bf["H"] + bf["s"] + bf["x"]
+    R = max(2, math.ceil(2 * L2_BYTES / per_set))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(SEED + 1000 * args.config + rank)
+    pts = torch.from_numpy(synth.QAM(cfg.M).points().astype("complex64")).to(dev)
+    Hs, Ss, Xs = [], [], []
+    for r in range(R):
+        h = torch.randn((cfg.n_sc, Bl, cfg.U, 2), generator=gen, device=dev) * math.sqrt(0.5)
+        Hs.append(torch.view_as_complex(h.contiguous()))
+        idx = torch.randint(0, cfg.M, (cfg.n_sc, cfg.K, cfg.U), generator=gen, device=dev)
+        Ss.append(pts[idx].contiguous())
+        Xs.append(torch.empty((cfg.n_sc, cfg.K, Bl), dtype=torch.complex64, device=dev))
+    stream = torch.cuda.current_stream(dev)
+
+    modes = ["pd", "fd"] if args.mode == "both" else [args.mode]
+
+    def step(i):
+        j = i % R
+        for m in modes:
+            fn = pre.precode_pd if m == "pd" else pre.precode_fd
+            fn(Hs[j], Ss[j], N0, 1.0, out=Xs[j])
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    pre.profile(reset=True)
+    if args.profile_run:
+        for i in range(args.steps):
+            step(i)
+        torch.cuda.synchronize(dev)
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "profile": pre.profile()}))
+        pre.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- timed region
+    launches0 = pre.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = pre.launch_count() - launches0
+    prof = pre.profile(reset=True)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    bits_frame = cfg.bits_per_frame
+    bits_step = bits_frame * len(modes)
+    value = bits_step * args.steps / (ms_max / 1e3) / 1e9
+
+    # ---------------- per-mode single-frame latency (p50 / p99 over 40 frames each)
+    lat = {}
+    for m in modes:
+        fn = pre.precode_pd if m == "pd" else pre.precode_fd
+        xs = []
+        for i in range(40):
+            j = i % R
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn(Hs[j], Ss[j], N0, 1.0, out=Xs[j])
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            tt = torch.tensor([a.elapsed_time(b)], device=dev)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            xs.append(float(tt.item()))
+        xs.sort()
+        p50 = xs[len(xs) // 2]
+        lat[m] = {"latency_ms_p50": p50, "latency_ms_p99": xs[min(len(xs) - 1, int(0.99 * len(xs)))],
+                  "gbps_at_p50": bits_frame / (p50 / 1e3) / 1e9}
+    pre.profile(reset=True)
+
+    # ---------------- e2e through the C-ABI with pinned HOST buffers (H2D + compute + D2H per call)
+    e2e = None
+    if not args.no_e2e:
+        Hh = Hs[0].cpu().pin_memory()
+        Sh = Ss[0].cpu().pin_memory()
+        Xh = torch.empty((cfg.n_sc, cfg.K, Bl), dtype=torch.complex64).pin_memory()
+        for m in modes:  # warm the staging buffers
+            (pre.precode_pd if m == "pd" else pre.precode_fd)(Hh, Sh, N0, 1.0, out=Xh)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ne = max(3, min(args.steps, 20))
+        e0.record(stream)
+        for i in range(ne):
+            for m in modes:
+                (pre.precode_pd if m == "pd" else pre.precode_fd)(Hh, Sh, N0, 1.0, out=Xh)
+        e1.record(stream)
+        barrier()
+        et = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        e2e = {"value": bits_step * ne / (e_ms / 1e3) / 1e9, "unit": "Gbit/s",
+               "h2d_bytes_per_step": len(modes) * (bf["H"] + bf["s"]),
+               "d2h_bytes_per_step": len(modes) * bf["x"], "ms_per_step": e_ms / ne,
+               "note": "pinned host H, s, x through dp_precode_*: H2D, kernels, D2H inside each call"}
+        pre.profile(reset=True)
+
+    # ---------------- roofline of the dominant kernel (measured in the timed region)
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    dom_ms = prof[dom]["ms"] / max(prof[dom]["launches"], 1)
+    step_ms_local = ms / args.steps
+    share = prof[dom]["ms"] / max(ms, 1e-9)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12            # TFLOP/s, FFMA pipe
+    Cl = cfg.C // world
+    if dom == "fused_fd":
+        fl = flops_problem(cfg.U, cfg.S, cfg.K)
+        flops_launch = cfg.n_sc * Cl * sum(fl.values())
+        bytes_launch = bf["H"] + bf["s"] + bf["x"]
+    elif dom in ("fused_pd", "solve_precode"):
+        fl = flops_problem(cfg.U, Bl, cfg.K)
+        flops_launch = cfg.n_sc * (sum(fl.values()) if dom == "fused_pd" else fl["solve"] + fl["whiten"] + fl["precode"])
+        bytes_launch = bf["H"] + bf["s"] + bf["x"]
+    else:
+        fl = flops_problem(cfg.U, Bl, cfg.K)
+        flops_launch = cfg.n_sc * fl.get(dom, sum(fl.values()))
+        bytes_launch = bf["H"]
+    achieved = flops_launch / (dom_ms / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(f"{cfg.name}/{dom}/n{world}")
+    except Exception:
+        pass
+    roof = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp32_peak, "traffic": traffic, "kernel": dom,
+            "kernel_ms_avg": dom_ms, "kernel_share_of_step": share,
+            "algorithmic_flops_per_launch": flops_launch, "algorithmic_bytes_per_launch": bytes_launch,
+            "hbm_achieved_gbs": bytes_launch / (dom_ms / 1e3) / 1e9,
+            "hbm_peak_gbs": peaks.get("hbm_gbs", 6544.0),
+            "peak_note": f"FP32 FFMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json)",
+            "kernels": {k: {"ms_avg": v["ms"] / max(v["launches"], 1), "launches": v["launches"]}
+                        for k, v in prof.items() if v["launches"]}}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(cfg, args.cpu_seconds)
+        cpu.pop("seconds", None)
+        cpu.pop("subcarriers", None)
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "complex64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: B={cfg.B} U={cfg.U} C={cfg.C} S={cfg.S} N_sc={cfg.n_sc} "
+                                   f"K={cfg.K} {cfg.M}-QAM SNR={cfg.snr_db} dB tau={cfg.tau}",
+                       "step": "+".join(m.upper() + "-WF frame" for m in modes),
+                       "bits_per_step": bits_step, "clusters_per_gpu": Cl,
+                       "parallelism": f"cluster-sharded x{world}" + ("" if world == 1 else f", PD {args.pd_topology}"),
+                       "l2": f"{R} rotating resident input sets of {per_set / 2**20:.1f} MiB (> 2x L2)",
+                       "path": "unfused (a)(b)(c)" if args.unfused else "fused single pass"},
+            "modes": lat,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "gpu_name": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(line), flush=True)
+    pre.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -107,10 +107,11 @@ template <int KC> struct ZL {
 
 // ------------------------------------------------------------------ (a) Gram
 // Column l of the Gram of rows [0, nrows) of a tile: acc[u] += h_b[u] conj(h_b[l]).
+// Rows are absolute tile rows (the swizzle phase depends on the row index).
 template <int U>
-__device__ __forceinline__ void gram_sg(const float2 *tile, int nrows, int l, float2 (&acc)[U]) {
+__device__ __forceinline__ void gram_sg(const float2 *tile, int row0, int nrows, int l, float2 (&acc)[U]) {
 #pragma unroll 2
-  for (int b = 0; b < nrows; ++b) {
+  for (int b = row0; b < row0 + nrows; ++b) {
     const float2 own = tile_elem<U>(tile, b, l);
 #pragma unroll
     for (int c = 0; c < U / 2; ++c) {
@@ -236,8 +237,9 @@ __device__ __forceinline__ void whiten_sg(const float2 (&d)[U], float ib, const 
 // ------------------------------------------------------------------ (c) precode
 // x[k][b] = sum_u conj(H[b][u]) z[k][u] for rows b = l, l+U, ... < nrows of a tile.
 // Writes x[k * xstride + b]; returns the lane's sum of |x|^2.
+// Rows are absolute tile rows row0 + r; x is indexed by r.
 template <int U, int KC>
-__device__ __forceinline__ float precode_sg(const float2 *tile, int nrows, const float2 *zT, int K,
+__device__ __forceinline__ float precode_sg(const float2 *tile, int row0, int nrows, const float2 *zT, int K,
                                             float2 *__restrict__ x, size_t xstride, int l) {
   constexpr int KCP = ZL<KC>::KCP;
   const int zs = ZL<KC>::zs(K);
@@ -249,7 +251,7 @@ __device__ __forceinline__ float precode_sg(const float2 *tile, int nrows, const
       for (int j = 0; j < KC; ++j) acc[j] = make_float2(0.f, 0.f);
 #pragma unroll 4
       for (int c = 0; c < U / 2; ++c) {
-        const float4 h = tile_chunk<U>(tile, b, c);
+        const float4 h = tile_chunk<U>(tile, row0 + b, c);
         const float2 h0 = make_float2(h.x, h.y), h1 = make_float2(h.z, h.w);
         const float2 *z0 = zT + (2 * c) * zs + q * KCP;   // z[.][2c], broadcast within the SG
         const float2 *z1 = z0 + zs;                        // z[.][2c+1]
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(256) fd_fused_kernel(Args a) {
   float2 acc[U];
 #pragma unroll
   for (int i = 0; i < U; ++i) acc[i] = make_float2(0.f, 0.f);
-  gram_sg<U>(tile, a.S, l, acc);
+  gram_sg<U>(tile, 0, a.S, l, acc);
 #pragma unroll
   for (int i = 0; i < U; ++i)
     if (i == l) { acc[i].x += a.kappa; acc[i].y = 0.f; }
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(256) fd_fused_kernel(Args a) {
   __syncwarp();
   float pw = 0.f;
   if (active)
-    pw = precode_sg<U, KC>(tile, a.S, scr, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
+    pw = precode_sg<U, KC>(tile, 0, a.S, scr, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
                            (size_t)a.Bl, l);
   pw = sg_sum<U>(pw);
   if (active && l == 0) {
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(256) sc_kernel(Args a) {
     float2 acc[U];
 #pragma unroll
     for (int i = 0; i < U; ++i) acc[i] = make_float2(0.f, 0.f);
-    if (sg < a.nchunks) gram_sg<U>(tile + (size_t)sg * a.S * U, a.S, l, acc);
+    if (sg < a.nchunks) gram_sg<U>(tile, sg * a.S, a.S, l, acc);
     if (MODE == MODE_GRAM && PER_CHUNK) {
       if (sg < a.nchunks) {
         float2 *out = a.Gout + ((size_t)sc * a.nchunks + sg) * npacked(U);
@@ -505,7 +507,7 @@ __global__ void __launch_bounds__(256) sc_kernel(Args a) {
   float pw = 0.f;
   if (sg < a.nchunks) {
     const int g = (MODE == MODE_PRECODE && zg > 1) ? sg / a.chunks_per_zgroup : 0;
-    pw = precode_sg<U, KC>(tile + (size_t)sg * a.S * U, a.S, zT + (size_t)g * U * zs, a.K,
+    pw = precode_sg<U, KC>(tile, sg * a.S, a.S, zT + (size_t)g * U * zs, a.K,
                            a.x + (size_t)sc * a.K * a.Bl + (size_t)sg * a.S, (size_t)a.Bl, l);
   }
   pw = sg_sum<U>(pw);
