@@ -363,14 +363,15 @@ def main():
         fl = flops_problem(cfg.U, cfg.S, cfg.K)
         flops_launch = cfg.n_sc * Cl * sum(fl.values())
         bytes_launch = bf["H"] + bf["s"] + bf["x"]
-    elif dom in ("fused_pd", "solve_precode"):
-        fl = flops_problem(cfg.U, Bl, cfg.K)
-        flops_launch = cfg.n_sc * (sum(fl.values()) if dom == "fused_pd" else fl["solve"] + fl["whiten"] + fl["precode"])
-        bytes_launch = bf["H"] + bf["s"] + bf["x"]
     else:
+        # PD kernels (a) gram: H -> packed G ; (b) solve: G, s -> z ; (c) precode: H, z -> x
         fl = flops_problem(cfg.U, Bl, cfg.K)
-        flops_launch = cfg.n_sc * fl.get(dom, sum(fl.values()))
-        bytes_launch = bf["H"]
+        npk = cfg.U * (cfg.U + 1) // 2 * 8
+        flops_launch = cfg.n_sc * {"gram": fl["gram"], "solve": fl["solve"] + fl["whiten"],
+                                   "precode": fl["precode"]}.get(dom, sum(fl.values()))
+        bytes_launch = {"gram": bf["H"] + cfg.n_sc * npk,
+                        "solve": cfg.n_sc * npk + bf["s"] + bf["s"],
+                        "precode": bf["H"] + bf["s"] + bf["x"]}.get(dom, bf["H"])
     achieved = flops_launch / (dom_ms / 1e3) / 1e12
     traffic = None
     try:

@@ -98,25 +98,57 @@ int next_pow2(int v) {
   return p;
 }
 
-int kc_of(int K) { return (K % 7 == 0) ? 7 : 8; }
+// precode/whitening symbol chunk KC: one chunk for K <= 16 (7, 8, 14 or 16), else chunks of 16
+int kc_of(int K) { return K == 7 ? 7 : K == 14 ? 14 : K <= 8 ? 8 : 16; }
 
 template <int KC>
 int zs_of(int K) { return dpk::ZL<KC>::zs(K); }
-int zs_rt(int K) { return kc_of(K) == 7 ? zs_of<7>(K) : zs_of<8>(K); }
+int zs_rt(int K) {
+  switch (kc_of(K)) {
+    case 7: return zs_of<7>(K);
+    case 8: return zs_of<8>(K);
+    case 14: return zs_of<14>(K);
+    default: return zs_of<16>(K);
+  }
+}
+template <int U>
+int fd_scr_rt(int K) {
+  switch (kc_of(K)) {
+    case 7: return dpk::fd_scr_size<U, 7>(K);
+    case 8: return dpk::fd_scr_size<U, 8>(K);
+    case 14: return dpk::fd_scr_size<U, 14>(K);
+    default: return dpk::fd_scr_size<U, 16>(K);
+  }
+}
+template <int U>
+int solve_scr_rt(int K) {
+  switch (kc_of(K)) {
+    case 7: return dpk::solve_scr_size<U, 7>(K);
+    case 8: return dpk::solve_scr_size<U, 8>(K);
+    case 14: return dpk::solve_scr_size<U, 14>(K);
+    default: return dpk::solve_scr_size<U, 16>(K);
+  }
+}
+int fd_scr_u(int U, int K) {
+  return U == 4 ? fd_scr_rt<4>(K) : U == 8 ? fd_scr_rt<8>(K) : U == 16 ? fd_scr_rt<16>(K) : fd_scr_rt<32>(K);
+}
+int solve_scr_u(int U, int K) {
+  return U == 4 ? solve_scr_rt<4>(K) : U == 8 ? solve_scr_rt<8>(K) : U == 16 ? solve_scr_rt<16>(K)
+                                                                             : solve_scr_rt<32>(K);
+}
 
 // ---------------------------------------------------------------- smem sizes (bytes)
 size_t smem_fd_fused(int U, int S, int K, int nw) {
   const int PPW = 32 / U;
-  const int scr = std::max(U + U * (U + 2), U * zs_rt(K));
-  return (size_t)nw * PPW * (S * U + scr) * sizeof(float2);
+  return (size_t)nw * PPW * (S * U + fd_scr_u(U, K)) * sizeof(float2);
 }
-size_t smem_sc(int U, int Bl, int K, int nw, int zgroups) {
-  const int PPW = 32 / U;
-  size_t e = (size_t)Bl * U + (size_t)(nw / 2) * U * (U + 2) + (size_t)PPW * (U + U * (U + 2)) +
-             (size_t)zgroups * U * zs_rt(K);
-  return e * sizeof(float2);
+size_t smem_gram(int U, int Bl, int nw) {
+  return ((size_t)Bl * U + (size_t)(nw / 2) * 32 * (U / 2 + U / 4)) * sizeof(float2);
 }
-size_t smem_solve(int U) { return (size_t)4 * (32 / U) * (U + U * (U + 2)) * sizeof(float2); }
+size_t smem_solve(int U, int K) { return (size_t)4 * (32 / U) * solve_scr_u(U, K) * sizeof(float2); }
+size_t smem_precode(int U, int Bl, int K, int zgroups) {
+  return ((size_t)Bl * U + (size_t)zgroups * U * zs_rt(K)) * sizeof(float2);
+}
 
 // ---------------------------------------------------------------- profiling helpers
 cudaEvent_t take_event(dp_ctx *c) {
@@ -182,27 +214,39 @@ int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   return DP_OK;
 }
 
-template <int U, int KC, int MODE, bool PER_CHUNK>
-int launch_sc(dp_ctx *c, const Args &a, int nw, int kid, cudaStream_t st) {
-  const size_t sm = smem_sc(U, a.Bl, a.K, nw, MODE == dpk::MODE_PRECODE ? a.zgroups : 1);
-  auto kern = dpk::sc_kernel<U, KC, MODE, PER_CHUNK>;
-  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "per-subcarrier tile needs %zu B of shared memory", sm);
+template <int U, bool PER_CHUNK>
+int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
+  const size_t sm = smem_gram(U, a.Bl, nw);
+  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "Gram tile needs %zu B of shared memory", sm);
+  auto kern = dpk::gram_kernel<U, PER_CHUNK>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  LaunchScope ls(c, kid, st);
+  LaunchScope ls(c, DP_KERNEL_GRAM, st);
   kern<<<a.n_sc, nw * 32, sm, st>>>(a);
   CK(cudaGetLastError());
   return DP_OK;
 }
 
-template <int U>
+template <int U, int KC>
 int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int per = 4 * (32 / U);
   const int nprob = a.n_sc * a.groups;
-  const size_t sm = smem_solve(U);
-  auto kern = dpk::solve_kernel<U>;
+  const size_t sm = smem_solve(U, a.K);
+  auto kern = dpk::solve_kernel<U, KC>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_SOLVE, st);
   kern<<<(nprob + per - 1) / per, 128, sm, st>>>(a);
+  CK(cudaGetLastError());
+  return DP_OK;
+}
+
+template <int U, int KC>
+int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
+  const size_t sm = smem_precode(U, a.Bl, a.K, a.zgroups);
+  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "precode tile needs %zu B of shared memory", sm);
+  auto kern = dpk::precode_kernel<U, KC>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  LaunchScope ls(c, DP_KERNEL_PRECODE, st);
+  kern<<<a.n_sc, nw * 32, sm, st>>>(a);
   CK(cudaGetLastError());
   return DP_OK;
 }
@@ -216,14 +260,22 @@ int launch_finish(dp_ctx *c, const float *beta, int nbeta, const float *pw, int 
 }
 
 // ---------------------------------------------------------------- U / KC dispatch
+template <template <int, int> class F, int U, typename... T>
+int dispatch_kc(int K, T... args) {
+  switch (kc_of(K)) {
+    case 7: return F<U, 7>::run(args...);
+    case 8: return F<U, 8>::run(args...);
+    case 14: return F<U, 14>::run(args...);
+    default: return F<U, 16>::run(args...);
+  }
+}
 template <template <int, int> class F, typename... T>
 int dispatch(int U, int K, T... args) {
-  const bool k7 = kc_of(K) == 7;
   switch (U) {
-    case 4: return k7 ? F<4, 7>::run(args...) : F<4, 8>::run(args...);
-    case 8: return k7 ? F<8, 7>::run(args...) : F<8, 8>::run(args...);
-    case 16: return k7 ? F<16, 7>::run(args...) : F<16, 8>::run(args...);
-    case 32: return k7 ? F<32, 7>::run(args...) : F<32, 8>::run(args...);
+    case 4: return dispatch_kc<F, 4>(K, args...);
+    case 8: return dispatch_kc<F, 8>(K, args...);
+    case 16: return dispatch_kc<F, 16>(K, args...);
+    case 32: return dispatch_kc<F, 32>(K, args...);
   }
   return fail(DP_ERR_UNSUPPORTED, "U=%d: kernels are instantiated for U in {4, 8, 16, 32}", U);
 }
@@ -231,33 +283,17 @@ int dispatch(int U, int K, T... args) {
 template <int U, int KC> struct FdFused {
   static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_fd_fused<U, KC>(c, a, st); }
 };
-template <int U, int KC> struct PdFused {
-  static int run(dp_ctx *c, Args a, cudaStream_t st) {
-    return launch_sc<U, KC, dpk::MODE_PD_FUSED, false>(c, a, c->pd_nw, DP_KERNEL_FUSED_PD, st);
-  }
-};
 template <int U, int KC> struct GramSum {
-  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) {
-    return launch_sc<U, 8, dpk::MODE_GRAM, false>(c, a, nw, DP_KERNEL_GRAM, st);
-  }
+  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) { return launch_gram<U, false>(c, a, nw, st); }
 };
 template <int U, int KC> struct GramPer {
-  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) {
-    return launch_sc<U, 8, dpk::MODE_GRAM, true>(c, a, nw, DP_KERNEL_GRAM, st);
-  }
-};
-template <int U, int KC> struct SolvePrecode {
-  static int run(dp_ctx *c, Args a, cudaStream_t st) {
-    return launch_sc<U, KC, dpk::MODE_SOLVE_PRECODE, false>(c, a, c->pd_nw, DP_KERNEL_SOLVE_PRECODE, st);
-  }
+  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) { return launch_gram<U, true>(c, a, nw, st); }
 };
 template <int U, int KC> struct Precode {
-  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) {
-    return launch_sc<U, KC, dpk::MODE_PRECODE, false>(c, a, nw, DP_KERNEL_PRECODE, st);
-  }
+  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) { return launch_precode<U, KC>(c, a, nw, st); }
 };
 template <int U, int KC> struct Solve {
-  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_solve<U>(c, a, st); }
+  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_solve<U, KC>(c, a, st); }
 };
 
 // ---------------------------------------------------------------- helpers
@@ -416,7 +452,7 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   // per-subcarrier PD kernels: split clusters into chunks (>= U rows) until the
   // CTA has >= 256 threads of SGs
   int chunk = S;
-  while ((c->Bl / chunk) * k.U < 256 && chunk % 2 == 0 && chunk / 2 >= k.U) chunk /= 2;
+  while ((c->Bl / chunk) * k.U < 256 && chunk % 16 == 0 && chunk / 2 >= k.U) chunk /= 2;
   c->pd_chunk = chunk;
   c->pd_nchunks = c->Bl / chunk;
   c->pd_nw = next_pow2((c->pd_nchunks * k.U + 31) / 32);
@@ -532,47 +568,33 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   const float2 *s_use = sd;
   if (!topo_t1) RET(distribute_s(c, sd, st, &s_use));   // T2: overlaps nothing yet; only s crosses
   a.s = s_use;
-  if (!c->comm_on) {
-    if (k.flags & DP_FLAG_UNFUSED) {
-      a.Gout = c->G;
-      RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
-      a.G = c->G;
-      a.zout = c->z;
-      RET(dispatch<Solve>(k.U, k.K, c, a, st));
-      a.zin = c->z;
-      a.zgroups = 1;
-      a.chunks_per_zgroup = c->pd_nchunks;
-      RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
-    } else {
-      RET(dispatch<PdFused>(k.U, k.K, c, a, st));
-    }
-  } else {
-    const size_t nG = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
-    // (a) local Gram: sum over this rank's clusters (the first adder-tree level)
-    a.Gout = c->G;
-    RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
-    a.G = c->G;
-    if (!topo_t1) {
-      // cross-rank adder tree G = sum_c G_c on every rank, then solve + precode in one pass
-      NK(ncclAllReduce(c->G, c->G, nG, ncclFloat, ncclSum, c->comm, st));
-      RET(dispatch<SolvePrecode>(k.U, k.K, c, a, st));
-    } else {
-      // paper topology: reduce to the master, master whitens, broadcast z
-      NK(ncclReduce(c->G, c->G, nG, ncclFloat, ncclSum, 0, c->comm, st));
-      if (k.rank == 0) {
-        a.zout = c->z;
-        RET(dispatch<Solve>(k.U, k.K, c, a, st));
-      }
-      NK(ncclGroupStart());
-      NK(ncclBroadcast(c->z, c->z, (size_t)k.n_sc * k.K * k.U * 2, ncclFloat, 0, c->comm, st));
-      NK(ncclBroadcast(c->beta, c->beta, (size_t)k.n_sc, ncclFloat, 0, c->comm, st));
-      NK(ncclGroupEnd());
-      a.zin = c->z;
-      a.zgroups = 1;
-      a.chunks_per_zgroup = c->pd_nchunks;
-      RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
-    }
+  // (a) Gram of this rank's antennas: first levels of the adder tree G = sum_c G_c
+  const size_t nG = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
+  a.Gout = c->G;
+  RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
+  a.G = c->G;
+  a.zout = c->z;
+  if (c->comm_on && !topo_t1) {
+    // cross-rank adder tree on every rank; every rank whitens redundantly
+    NK(ncclAllReduce(c->G, c->G, nG, ncclFloat, ncclSum, c->comm, st));
+  } else if (topo_t1) {
+    // paper topology: reduce the Grams to the master GPU
+    NK(ncclReduce(c->G, c->G, nG, ncclFloat, ncclSum, 0, c->comm, st));
   }
+  // (b) whitening node: A = G + kappa I, LDL^H, A^{-1}, beta (Lemma 1), z = A^{-1} s / beta
+  if (!topo_t1 || k.rank == 0) RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  if (topo_t1) {
+    // master broadcasts z and beta
+    NK(ncclGroupStart());
+    NK(ncclBroadcast(c->z, c->z, (size_t)k.n_sc * k.K * k.U * 2, ncclFloat, 0, c->comm, st));
+    NK(ncclBroadcast(c->beta, c->beta, (size_t)k.n_sc, ncclFloat, 0, c->comm, st));
+    NK(ncclGroupEnd());
+  }
+  // (c) local precode x_c = H_c^H z on every rank
+  a.zin = c->z;
+  a.zgroups = 1;
+  a.chunks_per_zgroup = c->pd_nchunks;
+  RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
   // per-subcarrier scalars: 1/beta contributed once (rank 0), power summed over ranks
   RET(launch_finish(c, c->beta, 1, c->pw, c->pd_nchunks, 0, st));
   if (c->comm_on) {

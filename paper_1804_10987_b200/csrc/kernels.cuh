@@ -4,19 +4,19 @@
 // Execution model.  All arithmetic is complex fp32 (the paper's
 // precision, cuBLAS C* routines).  The unit of work is a SUB-GROUP
 // (SG) of U consecutive lanes of a warp (U in {4, 8, 16, 32}; 32/U SGs per
-// warp).  Lane l of an SG owns column l of every U x U matrix of its problem,
-// kept in registers:
-//   gram_sg    G[:, l]  = sum_b h_b conj(h_b[l])                (G_c = H_c H_c^H)
-//   solve_sg   right-looking Cholesky A = L L^H
-//              forward substitution  W0 = L^{-1}
-//              back substitution     A^{-1} = W0^H W0
-//              beta from tr A^{-1} = ||W0||_F^2 and ||A^{-1}||_F^2 (Lemma 1, Eq. 6)
-//   whiten_sg  z_k[l] = sum_v conj(A^{-1}[v][l]) s_k[v] / beta
-//   precode_sg x_k[b] = sum_u conj(H[b][u]) z_k[u]               (x_c = H_c^H z)
-// H tiles live in shared memory with a 16-byte-chunk XOR swizzle so that both
-// access patterns are conflict-free: row broadcast (Gram) and one row per lane
-// (precode).  No atomics on data: every sum has a fixed order, so results are
-// bit-reproducible run to run.
+// warp).  Lane l of an SG owns column l of the U x U matrices of its problem:
+//   gram_sg    G = sum_b h_b h_b^H over a tile's rows, Hermitian-reduced
+//              (G_c = H_c H_c^H)
+//   solve_sg   A = G + kappa I = L D L^H (Cholesky in root-free LDL^H form,
+//              P:285), W0 = L^{-1} (forward substitution), A^{-1} =
+//              W0^H D^{-1} W0 (back substitution), and beta from
+//              tr A^{-1} and ||A^{-1}||_F^2 (Lemma 1, Eq. 6)
+//   whiten_sg  z_k = A^{-1} s_k / beta
+//   precode_sg x_k[b] = sum_u conj(H[b][u]) z_k[u]              (x_c = H_c^H z)
+// H tiles live in shared memory with a 16-byte-chunk XOR swizzle (period 8
+// rows) so that both access patterns are conflict-free: row broadcast (Gram)
+// and one row per lane (precode).  No atomics on data: every sum has a fixed
+// order, so results are bit-reproducible run to run.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -44,8 +44,12 @@ __device__ __forceinline__ void cfms(float2 &acc, float2 a, float2 b) {
   acc.x = fmaf(-a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
   acc.y = fmaf(-a.x, b.y, acc.y); acc.y = fmaf(-a.y, b.x, acc.y);
 }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float cabs2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 __device__ __forceinline__ float qnan() { return __int_as_float(0x7fc00000); }
+__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
 
 // sum over the U lanes of an SG (butterfly; every lane gets the total)
 template <int U>
@@ -57,23 +61,19 @@ __device__ __forceinline__ float sg_sum(float v) {
 
 // ------------------------------------------------------------------ swizzled H tile
 // Tile row b holds U complex = U/2 16-byte chunks; chunk c of row b is stored at
-// chunk position c ^ swz(b).  For every U, 8 consecutive rows read at one chunk
-// index land in 8 distinct 16-byte bank groups (precode: one row per lane), and
-// a row is still read as aligned float4 chunks (Gram: row broadcast).
+// chunk position c ^ swz(b).  swz has period 8 in b for every U; 8 consecutive
+// rows read at one chunk index land in 8 distinct 16-byte bank groups.
 template <int U>
-__device__ __forceinline__ int swz(int b) {
-  constexpr int CPR = U / 2;                      // chunks per row
-  constexpr int RPS = CPR >= 8 ? 1 : 8 / CPR;     // rows per 128-byte bank sweep
-  constexpr int NS = CPR >= 8 ? 8 : CPR;          // distinct swizzle values
-  return (b / RPS) % NS;
+__host__ __device__ constexpr int swz(int b) {
+  return (b / ((U / 2) >= 8 ? 1 : 8 / (U / 2))) % ((U / 2) >= 8 ? 8 : (U / 2));
 }
 template <int U>
-__device__ __forceinline__ float4 tile_chunk(const float2 *tile, int b, int c) {
-  return *reinterpret_cast<const float4 *>(tile + (size_t)b * U + 2 * (c ^ swz<U>(b)));
+__device__ __forceinline__ float4 ld_chunk(const float2 *row, int c, int sw) {
+  return *reinterpret_cast<const float4 *>(row + 2 * (c ^ sw));
 }
 template <int U>
-__device__ __forceinline__ float2 tile_elem(const float2 *tile, int b, int u) {
-  return tile[(size_t)b * U + 2 * ((u >> 1) ^ swz<U>(b)) + (u & 1)];
+__device__ __forceinline__ float2 ld_elem(const float2 *row, int u, int sw) {
+  return row[2 * ((u >> 1) ^ sw) + (u & 1)];
 }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -95,6 +95,12 @@ __device__ __forceinline__ void load_tile_async(float2 *tile, const float2 *__re
   }
 }
 
+// Async copy of n complex (n even, 16-byte aligned) by the U lanes of an SG.
+template <int U>
+__device__ __forceinline__ void sg_copy_async(float2 *dst, const float2 *__restrict__ src, int n, int l) {
+  for (int i = l; i < n / 2; i += U) cp_async16(dst + 2 * i, src + 2 * i);
+}
+
 // ------------------------------------------------------------------ z layout
 // zT[u][k] with symbols grouped in chunks of KC, each chunk starting at an even
 // (16-byte aligned) offset: index(u, k) = u*zs + (k/KC)*KCP + k%KC.
@@ -106,19 +112,113 @@ template <int KC> struct ZL {
 };
 
 // ------------------------------------------------------------------ (a) Gram
-// Column l of the Gram of rows [0, nrows) of a tile: acc[u] += h_b[u] conj(h_b[l]).
-// Rows are absolute tile rows (the swizzle phase depends on the row index).
-template <int U>
-__device__ __forceinline__ void gram_sg(const float2 *tile, int row0, int nrows, int l, float2 (&acc)[U]) {
-#pragma unroll 2
-  for (int b = row0; b < row0 + nrows; ++b) {
-    const float2 own = tile_elem<U>(tile, b, l);
+// Hermitian-reduced assignment of G entries to the U lanes of an SG:
+//   top[r], r < U/2:  G[r][l]                        (rows 0..U/2-1, every column)
+//   br[r],  r < U/4:  G[U/2 + (U/4)h + r][U/2 + l']   (bottom-right block, split in two
+//                      row halves h = l / (U/2); column l' = l % (U/2))
+// 3U/4 entries per lane instead of U, every load a broadcast (two addresses per
+// warp for the bottom-right rows).  The lower-left block is (top-right)^H.
+template <int U> struct GAcc {
+  float2 top[U / 2];
+  float2 br[U / 4];
+  __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int c = 0; c < U / 2; ++c) {
-      const float4 h = tile_chunk<U>(tile, b, c);      // same address for the whole SG: broadcast
-      cfma_bc(acc[2 * c], make_float2(h.x, h.y), own);
-      cfma_bc(acc[2 * c + 1], make_float2(h.z, h.w), own);
+    for (int i = 0; i < U / 2; ++i) top[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < U / 4; ++i) br[i] = make_float2(0.f, 0.f);
+  }
+};
+
+template <int U>
+__device__ __forceinline__ void gram_row(const float2 *row, int sw, int l, GAcc<U> &g) {
+  constexpr int H2 = U / 2, Q = U / 4;
+  const int h = l / H2, lc = H2 + (l % H2);
+  const float2 own = ld_elem<U>(row, l, sw);        // h_b[l]
+  const float2 own2 = ld_elem<U>(row, lc, sw);      // h_b[U/2 + l']
+#pragma unroll
+  for (int c = 0; c < H2 / 2; ++c) {                // rows 0..U/2-1: broadcast
+    const float4 v = ld_chunk<U>(row, c, sw);
+    cfma_bc(g.top[2 * c], lo2(v), own);
+    cfma_bc(g.top[2 * c + 1], hi2(v), own);
+  }
+  if constexpr (Q >= 2) {
+#pragma unroll
+    for (int c = 0; c < Q / 2; ++c) {               // rows U/2 + Q h + .. : two addresses per warp
+      const float4 v = ld_chunk<U>(row, H2 / 2 + h * (Q / 2) + c, sw);
+      cfma_bc(g.br[2 * c], lo2(v), own2);
+      cfma_bc(g.br[2 * c + 1], hi2(v), own2);
     }
+  } else {                                          // U = 4: one bottom-right row per lane
+    cfma_bc(g.br[0], ld_elem<U>(row, H2 + h, sw), own2);
+  }
+}
+
+// Gram over tile rows [row0, row0 + nrows); with row0 % 8 == 0 the swizzle of
+// each 8-row group is a compile-time constant.
+template <int U>
+__device__ __forceinline__ void gram_sg(const float2 *tile, int row0, int nrows, int l, GAcc<U> &g) {
+  int b = row0;
+  const int end = row0 + nrows;
+  if ((row0 & 7) == 0)
+  for (; b + 8 <= end; b += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) gram_row<U>(tile + (size_t)(b + j) * U, swz<U>(j), l, g);
+  }
+  for (; b < end; ++b) gram_row<U>(tile + (size_t)b * U, swz<U>(b), l, g);
+}
+
+// Scatter a lane's entries into M[u][v] (row stride MS) and read back column l
+// of the full Hermitian G + kappa I.
+template <int U, int MS>
+__device__ __forceinline__ void gram_to_column(const GAcc<U> &g, float2 *M, int l, float kappa,
+                                               float2 (&a)[U]) {
+  constexpr int H2 = U / 2, Q = U / 4;
+  const int h = l / H2, lc = H2 + (l % H2);
+#pragma unroll
+  for (int r = 0; r < H2; ++r) M[r * MS + l] = g.top[r];
+#pragma unroll
+  for (int r = 0; r < Q; ++r) M[(H2 + Q * h + r) * MS + lc] = g.br[r];
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    float2 v;
+    if (u < H2 || l >= H2) v = M[u * MS + l];
+    else v = cconj(M[l * MS + u]);                  // lower-left block = (top-right)^H
+    if (u == l) { v.x += kappa; v.y = 0.f; }
+    a[u] = v;
+  }
+  __syncwarp();
+}
+
+// Upper-triangle packed index (u <= v, row-major).
+__host__ __device__ constexpr int npacked(int U) { return U * (U + 1) / 2; }
+__device__ __forceinline__ int pidx(int U, int u, int v) { return u * U - (u * (u - 1)) / 2 + (v - u); }
+
+// Write a lane's entries with u <= v to packed storage.
+template <int U>
+__device__ __forceinline__ void gram_store_packed(const GAcc<U> &g, float2 *out, int l) {
+  constexpr int H2 = U / 2, Q = U / 4;
+  const int h = l / H2, lc = H2 + (l % H2);
+#pragma unroll
+  for (int r = 0; r < H2; ++r)
+    if (r <= l) out[pidx(U, r, l)] = g.top[r];
+#pragma unroll
+  for (int r = 0; r < Q; ++r) {
+    const int u = H2 + Q * h + r;
+    if (u <= lc) out[pidx(U, u, lc)] = g.br[r];
+  }
+}
+
+// Column l of G + kappa I from packed upper-triangle storage.
+template <int U>
+__device__ __forceinline__ void load_packed_col(const float2 *Gp, int l, float kappa, float2 (&a)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    float2 g;
+    if (u <= l) g = Gp[pidx(U, u, l)];
+    else g = cconj(Gp[pidx(U, l, u)]);
+    if (u == l) { g.x += kappa; g.y = 0.f; }
+    a[u] = g;
   }
 }
 
@@ -128,10 +228,24 @@ template <int U> struct Scr {
   static constexpr int MS = U + 2;
   static constexpr int SIZE = U + U * MS;   // complex elements
 };
+// FD fused scratch per SG: [slot U][M region]; the M region first holds the Gram
+// columns (U x MS), then s (K x U, staged during the sweep) followed by zT.
+template <int U, int KC>
+__host__ __device__ inline int fd_scr_size(int K) {
+  const int m1 = U * (U + 2), m2 = K * U + U * ZL<KC>::zs(K);
+  return U + (m1 > m2 ? m1 : m2);
+}
+// solve kernel scratch per SG: [slot U][packed G][s K x U][zT U x zs]
+template <int U, int KC>
+__host__ __device__ inline int solve_scr_size(int K) {
+  return U + U * (U + 1) / 2 + K * U + U * ZL<KC>::zs(K);
+}
 
-// In: a[] = column l of A = G + kappa I (full Hermitian column, lane l of the SG).
-// Out: d[] = column l of A^{-1}; returns beta (Lemma 1).  ok = false if a Cholesky
-// pivot is not a finite positive number or beta's radicand is not.
+// In: a[] = column l of A = G + kappa I (full Hermitian column).
+// Out: d[] = column l of A^{-1}; returns beta (Lemma 1).  ok = false if a pivot
+// of A is not a finite positive number (A not HPD) or beta's radicand is not.
+// A = L D L^H with unit lower L: the root-free form of the Cholesky factor
+// L_chol = L D^{1/2}.  The pivot column broadcast uses Hermitian symmetry.
 template <int U>
 __device__ __forceinline__ float solve_sg(float2 (&a)[U], float2 (&d)[U], float2 *scr, int l,
                                           float kappa, float coef, bool &ok) {
@@ -139,56 +253,52 @@ __device__ __forceinline__ float solve_sg(float2 (&a)[U], float2 (&d)[U], float2
   float2 *M = scr + U;
   constexpr int MS = Scr<U>::MS;
   ok = true;
-  // ---- Cholesky, right-looking.  Lane l holds column l of the trailing matrix
-  // including its upper part, so lane i's a[k] = A^(k)[k][i] = conj(A^(k)[i][k]):
-  // publishing a[k] through `slot` broadcasts the pivot column.
+  // ---- LDL^H, right-looking.  Lane l holds column l of the trailing matrix incl.
+  // its upper part, so lane i's a[k] = A^(k)[k][i] = conj(A^(k)[i][k]).
 #pragma unroll
   for (int k = 0; k < U; ++k) {
     slot[l] = a[k];
     __syncwarp();
-    float dk = slot[k].x;                        // A^(k)[k][k]
+    float dk = slot[k].x;                                   // pivot d_k = A^(k)[k][k]
     const bool good = (dk > 0.f) && (dk < INFINITY);
     ok = ok && good;
     dk = good ? dk : 1.f;
-    // (constant trip counts with compile-time guards so that nvcc unrolls fully
-    // and a[] stays in registers)
     if (l > k) {
-      const float il2 = __fdividef(1.f, dk);
-      const float2 m = make_float2(a[k].x * il2, a[k].y * il2);  // conj(L[l][k]) / L[k][k]
+      const float2 m = cscale(a[k], __fdividef(1.f, dk));   // A^(k)[k][l] / d_k
 #pragma unroll
       for (int i = 0; i < U; ++i)
-        if (i > k) cfms_cj(a[i], slot[i], m);                      // a[i] -= L[i][k] conj(L[l][k])
-    } else if (l == k) {
-      const float il = rsqrtf(dk);
-#pragma unroll
-      for (int i = 0; i < U; ++i)
-        if (i > k) { a[i].x *= il; a[i].y *= il; }                 // L[i][k]
-      a[k] = make_float2(dk * il, 0.f);                            // L[k][k] = sqrt(dk)
+        if (i > k) cfms_cj(a[i], slot[i], m);               // a[i] -= A[i][k] A[k][l] / d_k
     }
+    if (l == k) a[k] = make_float2(dk, 0.f);
     __syncwarp();
   }
+  // M[k][i] = A^(k)[i][k] = d_k L[i][k] (i > k);  M[k][k] = d_k
 #pragma unroll
-  for (int i = 0; i < U; ++i) M[l * MS + i] = a[i];                   // M[k][i] = L[i][k], i >= k
+  for (int i = 0; i < U; ++i) M[l * MS + i] = a[i];
   __syncwarp();
-  // ---- forward substitution L X = I; lane l holds column l of X = L^{-1}
+  // ---- forward substitution L X = I (unit diagonal); lane l holds column l of W0 = L^{-1}
   float2 x[U];
 #pragma unroll
   for (int i = 0; i < U; ++i) x[i] = make_float2(i == l ? 1.f : 0.f, 0.f);
+  float t = 0.f;                                            // tr A^{-1} = sum_m |W0[m][l]|^2 / d_m
 #pragma unroll
   for (int k = 0; k < U; ++k) {
-    const float il = __fdividef(1.f, M[k * MS + k].x);
-    const float2 xk = make_float2(x[k].x * il, x[k].y * il);
-    x[k] = xk;
+    const float idk = __fdividef(1.f, M[k * MS + k].x);
+    const float2 sk = cscale(x[k], idk);                    // W0[k][l] / d_k
+    t = fmaf(sk.x, x[k].x, fmaf(sk.y, x[k].y, t));
+    if (l == k) slot[k] = make_float2(idk, 0.f);
 #pragma unroll
     for (int i = 0; i < U; ++i)
-      if (i > k) cfms(x[i], M[k * MS + i], xk);                       // x[i] -= L[i][k] x[k]
+      if (i > k) cfms(x[i], M[k * MS + i], sk);             // x[i] -= L[i][k] x[k]
   }
   __syncwarp();
-  float t = 0.f;                                                      // tr A^{-1} = ||L^{-1}||_F^2
+  // M[j][m] = W0[m][j] (lane j writes its column as row j), then x[m] <- W0[m][l] / d_m
 #pragma unroll
-  for (int i = 0; i < U; ++i) { t += cabs2(x[i]); M[l * MS + i] = x[i]; }   // M[j][i] = W0[i][j]
+  for (int i = 0; i < U; ++i) M[l * MS + i] = x[i];
   __syncwarp();
-  // ---- back substitution A^{-1} = L^{-H} L^{-1}:  d[u] = sum_{m>=u} conj(W0[m][u]) W0[m][l]
+#pragma unroll
+  for (int m = 0; m < U; ++m) x[m] = cscale(x[m], slot[m].x);
+  // ---- A^{-1} = W0^H D^{-1} W0:  d[u] = sum_{m >= u} conj(W0[m][u]) W0[m][l] / d_m
   float f = 0.f;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -209,61 +319,161 @@ __device__ __forceinline__ float solve_sg(float2 (&a)[U], float2 (&d)[U], float2
   return good ? sqrtf(r) : 1.f;
 }
 
+// In-place symmetric (Hermitian) Gauss-Jordan sweep: pivot k performs the k-th
+// step of the root-free Cholesky (LDL^H) elimination of the trailing block and,
+// in the same pass, the k-th forward/back substitution step on the block already
+// eliminated, so after U pivots w holds column l of -A^{-1} (Goodnight's sweep).
+// Every lane updates every row at every pivot (no triangular lockstep waste), and
+// the pivot column is broadcast through `slot` using Hermitian symmetry: lane i
+// publishes its row-k entry a_ki = conj(a_ik).  The runtime pivot loop keeps the
+// code small (instruction-cache resident): R pivots are unrolled per iteration and
+// the register column is rotated by R rows at the end of it, so the pivot row is
+// always a compile-time register.
+// In: w[] = column l of A = G + kappa I.  Out: w[] = column l of -A^{-1}; returns
+// beta (Lemma 1, Eq. 6); ok = false if a pivot is not finite and positive (A not
+// HPD) or beta's radicand is not.
+template <int U>
+__device__ __forceinline__ float sweep_sg(float2 (&w)[U], float2 *slot, int l, float kappa, float coef,
+                                          bool &ok) {
+  constexpr int R = U >= 4 ? 4 : U;
+  ok = true;
+  // ---- Jacobi equilibration A' = D^{-1/2} A D^{-1/2} (unit diagonal, pivots in (0, 1])
+  float dl = 0.f;
+#pragma unroll
+  for (int p = 0; p < U; ++p)
+    if (p == l) dl = w[p].x;
+  ok = (dl > 0.f) && (dl < INFINITY);
+  const float rl = ok ? rsqrtf(dl) : 1.f;
+  slot[l] = make_float2(rl, 0.f);
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < U; p += 2) {
+    const float4 r2 = *reinterpret_cast<const float4 *>(slot + p);
+    w[p] = cscale(w[p], r2.x * rl);
+    w[p + 1] = cscale(w[p + 1], r2.z * rl);
+  }
+  __syncwarp();
+  // ---- sweep
+#pragma unroll 1
+  for (int kk = 0; kk < U; kk += R) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int k = kk + j;                       // pivot (register position j holds row k)
+      slot[(l - kk) & (U - 1)] = w[j];            // a_kl, stored at the rotated position of lane l
+      __syncwarp();
+      float dk = slot[j].x;                       // a_kk
+      const bool good = (dk > 0.f) && (dk < INFINITY);
+      ok = ok && good;
+      dk = good ? dk : 1.f;
+      const float id = __fdividef(1.f, dk);
+      const bool piv = (l == k);
+      // Non-pivot lanes: a_pl -= a_pk a_kl / d.  The pivot lane's own column holds
+      // a_pk, the Hermitian mirror of the broadcast conj(a_kp), so sigma = 1 - 1/d
+      // turns it into a_pk / d (equal up to the rounding asymmetry of the mirrors,
+      // which the unit-diagonal scaling keeps at the level of the pivots' rounding).
+      const float2 sig = piv ? make_float2(1.f - id, 0.f) : cscale(w[j], id);
+#pragma unroll
+      for (int p = 0; p < U; p += 2) {
+        const float4 sv = *reinterpret_cast<const float4 *>(slot + p);
+        if (p != j) cfms_cj(w[p], lo2(sv), sig);
+        if (p + 1 != j) cfms_cj(w[p + 1], hi2(sv), sig);
+      }
+      w[j] = piv ? make_float2(-id, 0.f) : cscale(w[j], id);
+      __syncwarp();
+    }
+    float2 t[R];                                  // rotate rows up by R
+#pragma unroll
+    for (int q = 0; q < R; ++q) t[q] = w[q];
+#pragma unroll
+    for (int p = 0; p + R < U; ++p) w[p] = w[p + R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) w[U - R + q] = t[q];
+  }
+  // ---- undo the equilibration: A^{-1} = D^{-1/2} A'^{-1} D^{-1/2}
+  slot[l] = make_float2(rl, 0.f);
+  __syncwarp();
+  float tr = 0.f, f = 0.f;
+#pragma unroll
+  for (int p = 0; p < U; p += 2) {
+    const float4 r2 = *reinterpret_cast<const float4 *>(slot + p);
+    w[p] = cscale(w[p], r2.x * rl);
+    w[p + 1] = cscale(w[p + 1], r2.z * rl);
+    f += cabs2(w[p]) + cabs2(w[p + 1]);
+    if (p == l) tr = -w[p].x;                     // diagonal of A^{-1}
+    if (p + 1 == l) tr = -w[p + 1].x;
+  }
+  __syncwarp();
+  tr = sg_sum<U>(tr);
+  f = sg_sum<U>(f);
+  // Lemma 1, Eq. (6):  beta^2 = Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)
+  const float r = coef * (tr - kappa * f);
+  const bool good = (r > 0.f) && (r < INFINITY);
+  ok = ok && good;
+  return good ? sqrtf(r) : 1.f;
+}
+
 // ------------------------------------------------------------------ whitening
 // z_k[l] = ib * sum_v conj(d[v]) s_k[v]  (d = column l of Hermitian A^{-1}, so
 // conj(d[v]) = A^{-1}[l][v]).  Written to zT for k in [kbeg, nkc*KC) step kstep,
-// zeros for k >= K.
+// zeros for k >= K.  Two symbols per iteration for independent FMA chains.
 template <int U, int KC>
-__device__ __forceinline__ void whiten_sg(const float2 (&d)[U], float ib, const float2 *__restrict__ s,
+__device__ __forceinline__ void whiten_sg(const float2 (&d)[U], float ib, const float2 *s,
                                           int K, int kbeg, int kstep, float2 *zT, int l) {
   const int zs = ZL<KC>::zs(K);
   const int kend = ZL<KC>::nkc(K) * KC;
-  for (int k = kbeg; k < kend; k += kstep) {
-    float2 acc = make_float2(0.f, 0.f);
-    if (k < K) {
-      const float4 *sk = reinterpret_cast<const float4 *>(s + (size_t)k * U);
+  for (int k = kbeg; k < kend; k += 2 * kstep) {
+    const int k2 = k + kstep;
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+    const float4 *s0 = reinterpret_cast<const float4 *>(s + (size_t)min(k, K - 1) * U);
+    const float4 *s1 = reinterpret_cast<const float4 *>(s + (size_t)min(k2, K - 1) * U);
 #pragma unroll
-      for (int c = 0; c < U / 2; ++c) {
-        const float4 v = __ldg(sk + c);
-        cfma_cj(acc, d[2 * c], make_float2(v.x, v.y));
-        cfma_cj(acc, d[2 * c + 1], make_float2(v.z, v.w));
-      }
-      acc.x *= ib; acc.y *= ib;
+    for (int c = 0; c < U / 2; ++c) {
+      const float4 v = s0[c];
+      const float4 w = s1[c];
+      cfma_cj(a0, d[2 * c], lo2(v));
+      cfma_cj(a1, d[2 * c + 1], hi2(v));
+      cfma_cj(b0, d[2 * c], lo2(w));
+      cfma_cj(b1, d[2 * c + 1], hi2(w));
     }
-    zT[ZL<KC>::idx(zs, l, k)] = acc;
+    const float ia = k < K ? ib : 0.f, ibb = k2 < K ? ib : 0.f;
+    zT[ZL<KC>::idx(zs, l, k)] = make_float2((a0.x + a1.x) * ia, (a0.y + a1.y) * ia);
+    if (k2 < kend) zT[ZL<KC>::idx(zs, l, k2)] = make_float2((b0.x + b1.x) * ibb, (b0.y + b1.y) * ibb);
   }
 }
 
 // ------------------------------------------------------------------ (c) precode
-// x[k][b] = sum_u conj(H[b][u]) z[k][u] for rows b = l, l+U, ... < nrows of a tile.
-// Writes x[k * xstride + b]; returns the lane's sum of |x|^2.
-// Rows are absolute tile rows row0 + r; x is indexed by r.
+// x[k][r] = sum_u conj(H[row0 + r][u]) z[k][u] for r = l, l+U, ... < nrows.
+// Writes x[k * xstride + r]; returns the lane's sum of |x|^2.
 template <int U, int KC>
 __device__ __forceinline__ float precode_sg(const float2 *tile, int row0, int nrows, const float2 *zT, int K,
                                             float2 *__restrict__ x, size_t xstride, int l) {
   constexpr int KCP = ZL<KC>::KCP;
   const int zs = ZL<KC>::zs(K);
   float pw = 0.f;
-  for (int b = l; b < nrows; b += U) {
+  for (int r = l; r < nrows; r += U) {
+    const int b = row0 + r;
+    const float2 *row = tile + (size_t)b * U;
+    const int sw = swz<U>(b);
     for (int k0 = 0, q = 0; k0 < K; k0 += KC, ++q) {
       float2 acc[KC];
 #pragma unroll
       for (int j = 0; j < KC; ++j) acc[j] = make_float2(0.f, 0.f);
+      const float2 *zq = zT + q * KCP;
 #pragma unroll 4
       for (int c = 0; c < U / 2; ++c) {
-        const float4 h = tile_chunk<U>(tile, row0 + b, c);
-        const float2 h0 = make_float2(h.x, h.y), h1 = make_float2(h.z, h.w);
-        const float2 *z0 = zT + (2 * c) * zs + q * KCP;   // z[.][2c], broadcast within the SG
+        const float4 h = ld_chunk<U>(row, c, sw);
+        const float2 h0 = lo2(h), h1 = hi2(h);
+        const float2 *z0 = zq + (2 * c) * zs;              // z[.][2c], broadcast within the SG
         const float2 *z1 = z0 + zs;                        // z[.][2c+1]
 #pragma unroll
         for (int j = 0; j < KC; j += 2) {
           if (j + 1 < KC) {
             const float4 za = *reinterpret_cast<const float4 *>(z0 + j);
             const float4 zb = *reinterpret_cast<const float4 *>(z1 + j);
-            cfma_cj(acc[j], h0, make_float2(za.x, za.y));
-            cfma_cj(acc[j + 1], h0, make_float2(za.z, za.w));
-            cfma_cj(acc[j], h1, make_float2(zb.x, zb.y));
-            cfma_cj(acc[j + 1], h1, make_float2(zb.z, zb.w));
+            cfma_cj(acc[j], h0, lo2(za));
+            cfma_cj(acc[j + 1], h0, hi2(za));
+            cfma_cj(acc[j], h1, lo2(zb));
+            cfma_cj(acc[j + 1], h1, hi2(zb));
           } else {
             cfma_cj(acc[j], h0, z0[j]);
             cfma_cj(acc[j], h1, z1[j]);
@@ -273,7 +483,7 @@ __device__ __forceinline__ float precode_sg(const float2 *tile, int row0, int nr
 #pragma unroll
       for (int j = 0; j < KC; ++j) {
         if (k0 + j < K) {
-          x[(size_t)(k0 + j) * xstride + b] = acc[j];
+          x[(size_t)(k0 + j) * xstride + r] = acc[j];
           pw += cabs2(acc[j]);
         }
       }
@@ -287,7 +497,7 @@ struct Args {
   const float2 *H;      // H_local [n_sc][Bl][U]
   const float2 *s;      // s [n_sc][K][U]
   float2 *x;            // x_local [n_sc][K][Bl]
-  const float2 *G;      // packed Gram input  [n_sc][groups][U(U+1)/2]  (solve kernels)
+  const float2 *G;      // packed Gram input  [n_sc][groups][U(U+1)/2]  (solve kernel)
   float2 *Gout;         // packed Gram output [n_sc][groups][U(U+1)/2]  (gram kernel)
   const float2 *zin;    // z input  [n_sc][zgroups][K][U]                (precode kernel)
   float2 *zout;         // z output [n_sc][groups][K][U]                 (solve kernel)
@@ -302,31 +512,14 @@ struct Args {
   float kappa, coef;    // regulariser and Es / rho_x^2
 };
 
-__host__ __device__ constexpr int npacked(int U) { return U * (U + 1) / 2; }
-__device__ __forceinline__ int pidx(int U, int u, int v) {   // u <= v, row-major upper triangle
-  return u * U - (u * (u - 1)) / 2 + (v - u);
-}
-// column l of G + kappa I from packed upper-triangle storage
-template <int U>
-__device__ __forceinline__ void load_packed_col(const float2 *Gp, int l, float kappa, float2 (&acc)[U]) {
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    float2 g;
-    if (u <= l) g = Gp[pidx(U, u, l)];
-    else { g = Gp[pidx(U, l, u)]; g.y = -g.y; }
-    if (u == l) { g.x += kappa; g.y = 0.f; }
-    acc[u] = g;
-  }
-}
-
 // ================================================================== FD fused kernel
 // One SG per (subcarrier, cluster) problem, NSG = (blockDim/32)*(32/U) problems per
 // CTA with consecutive problem ids (= consecutive antenna rows of H_local).  Single
-// pass over H: cp.async tile -> Gram -> +kappa_c -> Cholesky -> L^{-1} -> A^{-1}
+// pass over H: cp.async tile -> Gram -> +kappa_c -> LDL^H -> L^{-1} -> A^{-1}
 // -> beta_c -> z = A^{-1} s / beta_c -> x_c = H_c^H z -> power partial.
 // smem per SG: tile S*U + scratch max(Scr::SIZE, U*zs).
 template <int U, int KC>
-__global__ void __launch_bounds__(256) fd_fused_kernel(Args a) {
+__global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
   const int nw = blockDim.x >> 5;
@@ -336,8 +529,7 @@ __global__ void __launch_bounds__(256) fd_fused_kernel(Args a) {
   const int nprob = a.n_sc * a.nchunks;
   const int p0 = blockIdx.x * NSG;
   const int np = min(NSG, nprob - p0);
-  const int zs = ZL<KC>::zs(a.K);
-  const int scr_sz = max(Scr<U>::SIZE, U * zs);
+  const int scr_sz = fd_scr_size<U, KC>(a.K);
   const int tile_sz = a.S * U;
   float2 *tile = smem + (size_t)sg * (tile_sz + scr_sz);
   float2 *scr = tile + tile_sz;
@@ -349,28 +541,32 @@ __global__ void __launch_bounds__(256) fd_fused_kernel(Args a) {
     cp_async_wait_all();
     __syncthreads();
   }
-  // Inactive SGs (tail CTA) run the warp-synchronous code on a clamped problem
-  // and write nothing.
+  // Inactive SGs (tail CTA) run the warp-synchronous code on SG 0's data and write nothing.
   const bool active = sg < np;
   const int p = active ? p0 + sg : p0;
-  if (!active) tile = smem;   // valid, loaded data
+  if (!active) tile = smem;
   const int sc = p / a.nchunks, cl = p % a.nchunks;
-  float2 acc[U];
-#pragma unroll
-  for (int i = 0; i < U; ++i) acc[i] = make_float2(0.f, 0.f);
-  gram_sg<U>(tile, 0, a.S, l, acc);
-#pragma unroll
-  for (int i = 0; i < U; ++i)
-    if (i == l) { acc[i].x += a.kappa; acc[i].y = 0.f; }
-  float2 d[U];
+  float2 *slot = scr, *Mreg = scr + U;
+  float2 col[U];
+  {
+    GAcc<U> g;
+    g.zero();
+    gram_sg<U>(tile, 0, a.S, l, g);
+    gram_to_column<U, Scr<U>::MS>(g, Mreg, l, a.kappa, col);
+  }
+  // stage s_k of this subcarrier into the (now free) M region while the sweep runs
+  sg_copy_async<U>(Mreg, a.s + (size_t)sc * a.K * U, a.K * U, l);
   bool ok;
-  const float beta = solve_sg<U>(acc, d, scr, l, a.kappa, a.coef, ok);
-  const float ib = ok ? __fdividef(1.f, beta) : 0.f;   // failed problems output x = 0
-  whiten_sg<U, KC>(d, ib, a.s + (size_t)sc * a.K * U, a.K, 0, 1, scr, l);
+  const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+  const float ib = ok ? -__fdividef(1.f, beta) : 0.f;   // sign folds -A^{-1}; failed problems: x = 0
+  cp_async_wait_all();
+  __syncwarp();
+  float2 *zT = Mreg + a.K * U;
+  whiten_sg<U, KC>(col, ib, Mreg, a.K, 0, 1, zT, l);
   __syncwarp();
   float pw = 0.f;
   if (active)
-    pw = precode_sg<U, KC>(tile, 0, a.S, scr, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
+    pw = precode_sg<U, KC>(tile, 0, a.S, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
                            (size_t)a.Bl, l);
   pw = sg_sum<U>(pw);
   if (active && l == 0) {
@@ -380,144 +576,71 @@ __global__ void __launch_bounds__(256) fd_fused_kernel(Args a) {
   }
 }
 
-// ================================================================== per-subcarrier CTA kernels
-// One CTA per subcarrier; SG g handles chunk g (rows [g*S, (g+1)*S) of H_local[sc]).
-// MODE_GRAM:          tile -> Gram per chunk -> (per chunk | adder tree) -> packed G out
-// MODE_PD_FUSED:      tile -> Gram -> adder tree -> warp 0: solve + whiten -> precode
-// MODE_SOLVE_PRECODE: packed G in -> warp 0: solve + whiten ; tile -> precode
-// MODE_PRECODE:       z in (per z group) ; tile -> precode
-// smem: [tile Bl*U][tree (nw/2)*U*MS][scr PPW*Scr::SIZE][zT zgroups*U*zs]
-enum { MODE_GRAM = 0, MODE_PD_FUSED = 1, MODE_SOLVE_PRECODE = 2, MODE_PRECODE = 3 };
-
-template <int U, int KC, int MODE, bool PER_CHUNK>
-__global__ void __launch_bounds__(256) sc_kernel(Args a) {
+// ================================================================== (a) Gram kernel
+// One CTA per subcarrier; SG g computes the Gram of chunk g (rows [g*S, (g+1)*S)
+// of H_local[sc]).  PER_CHUNK: packed Gram per chunk.  Otherwise the feedforward
+// adder tree G = sum_c G_c: over the SGs of a warp (butterfly), then across
+// warps through shared memory, in a fixed order; packed G out.
+// smem: [tile Bl*U][tree (nw/2) * 32 * (3U/4) complex]
+template <int U, bool PER_CHUNK>
+__global__ void __launch_bounds__(256) gram_kernel(Args a) {
   constexpr int PPW = 32 / U;
-  constexpr int MS = Scr<U>::MS;
+  constexpr int NE = U / 2 + U / 4;
   extern __shared__ __align__(16) float2 smem[];
   const int nw = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sg = warp * PPW + lane / U, l = lane % U;
   const int sc = blockIdx.x;
-  const int zs = ZL<KC>::zs(a.K);
-  const int zg = (MODE == MODE_PRECODE) ? a.zgroups : 1;
   float2 *tile = smem;
   float2 *tree = tile + (size_t)a.Bl * U;
-  float2 *scr = tree + (size_t)(nw / 2) * U * MS;
-  float2 *zT = scr + (size_t)PPW * Scr<U>::SIZE;
   load_tile_async<U>(tile, a.H + (size_t)sc * a.Bl * U, a.Bl, threadIdx.x, blockDim.x);
-  if (MODE == MODE_PRECODE) {
-    const float2 *src = a.zin + (size_t)sc * zg * a.K * U;     // z[sc][g][k][u] -> zT[g]
-    const int kend = ZL<KC>::nkc(a.K) * KC;
-    for (int i = threadIdx.x; i < zg * U * kend; i += blockDim.x) {
-      const int g = i / (U * kend), r = i % (U * kend), u = r / kend, k = r % kend;
-      zT[(size_t)g * U * zs + ZL<KC>::idx(zs, u, k)] =
-          (k < a.K) ? src[((size_t)g * a.K + k) * U + u] : make_float2(0.f, 0.f);
-    }
-  }
   cp_async_wait_all();
   __syncthreads();
-
-  if (MODE == MODE_GRAM || MODE == MODE_PD_FUSED) {
-    float2 acc[U];
+  GAcc<U> g;
+  g.zero();
+  if (sg < a.nchunks) gram_sg<U>(tile, sg * a.S, a.S, l, g);
+  if constexpr (PER_CHUNK) {
+    if (sg < a.nchunks) gram_store_packed<U>(g, a.Gout + ((size_t)sc * a.nchunks + sg) * npacked(U), l);
+  } else {
 #pragma unroll
-    for (int i = 0; i < U; ++i) acc[i] = make_float2(0.f, 0.f);
-    if (sg < a.nchunks) gram_sg<U>(tile, sg * a.S, a.S, l, acc);
-    if (MODE == MODE_GRAM && PER_CHUNK) {
-      if (sg < a.nchunks) {
-        float2 *out = a.Gout + ((size_t)sc * a.nchunks + sg) * npacked(U);
+    for (int m = U; m < 32; m <<= 1) {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (u <= l) out[pidx(U, u, l)] = acc[u];
+      for (int i = 0; i < U / 2; ++i) {
+        g.top[i].x += __shfl_xor_sync(0xffffffffu, g.top[i].x, m);
+        g.top[i].y += __shfl_xor_sync(0xffffffffu, g.top[i].y, m);
       }
-      return;
+#pragma unroll
+      for (int i = 0; i < U / 4; ++i) {
+        g.br[i].x += __shfl_xor_sync(0xffffffffu, g.br[i].x, m);
+        g.br[i].y += __shfl_xor_sync(0xffffffffu, g.br[i].y, m);
+      }
     }
-    // feedforward adder tree G = sum_c G_c: over the SGs of a warp, then
-    // across warps, in a fixed order
-#pragma unroll
-    for (int m = U; m < 32; m <<= 1)
-#pragma unroll
-      for (int i = 0; i < U; ++i) {
-        acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, m);
-        acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, m);
-      }
     for (int half = nw / 2; half >= 1; half >>= 1) {
-      if (warp >= half && warp < 2 * half && lane < U) {
-        float2 *buf = tree + (size_t)(warp - half) * U * MS;
+      if (warp >= half && warp < 2 * half) {
+        float2 *buf = tree + ((size_t)(warp - half) * 32 + lane) * NE;
 #pragma unroll
-        for (int i = 0; i < U; ++i) buf[i * MS + l] = acc[i];
+        for (int i = 0; i < U / 2; ++i) buf[i] = g.top[i];
+#pragma unroll
+        for (int i = 0; i < U / 4; ++i) buf[U / 2 + i] = g.br[i];
       }
       __syncthreads();
-      if (warp < half && lane < U) {
-        const float2 *buf = tree + (size_t)warp * U * MS;
+      if (warp < half) {
+        const float2 *buf = tree + ((size_t)warp * 32 + lane) * NE;
 #pragma unroll
-        for (int i = 0; i < U; ++i) { acc[i].x += buf[i * MS + l].x; acc[i].y += buf[i * MS + l].y; }
+        for (int i = 0; i < U / 2; ++i) { g.top[i].x += buf[i].x; g.top[i].y += buf[i].y; }
+#pragma unroll
+        for (int i = 0; i < U / 4; ++i) { g.br[i].x += buf[U / 2 + i].x; g.br[i].y += buf[U / 2 + i].y; }
       }
       __syncthreads();
     }
-    if (MODE == MODE_GRAM) {
-      if (warp == 0 && lane < U) {
-        float2 *out = a.Gout + (size_t)sc * npacked(U);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (u <= l) out[pidx(U, u, l)] = acc[u];
-      }
-      return;
-    }
-    if (warp == 0) {
-      // all SGs of warp 0 hold G (lane l of each SG: column l); SG 0 is
-      // authoritative, the others redo the solve to share the whitening
-      // SGs > 0 of warp 0 hold only warp 0's partial sum: take SG 0's column l
-#pragma unroll
-      for (int i = 0; i < U; ++i) {
-        acc[i].x = __shfl_sync(0xffffffffu, acc[i].x, l);
-        acc[i].y = __shfl_sync(0xffffffffu, acc[i].y, l);
-      }
-#pragma unroll
-      for (int i = 0; i < U; ++i)
-        if (i == l) { acc[i].x += a.kappa; acc[i].y = 0.f; }
-      float2 d[U];
-      bool ok;
-      const float beta = solve_sg<U>(acc, d, scr + (size_t)(lane / U) * Scr<U>::SIZE, l, a.kappa, a.coef, ok);
-      const float ib = ok ? __fdividef(1.f, beta) : 0.f;
-      whiten_sg<U, KC>(d, ib, a.s + (size_t)sc * a.K * U, a.K, lane / U, PPW, zT, l);
-      if (lane == 0) {
-        a.beta[sc] = ok ? beta : qnan();
-        if (!ok) atomicAdd(a.bad, 1);
-      }
-    }
-    __syncthreads();
+    if (warp == 0 && lane < U) gram_store_packed<U>(g, a.Gout + (size_t)sc * npacked(U), l);
   }
-  if (MODE == MODE_SOLVE_PRECODE) {
-    if (warp == 0) {
-      float2 acc[U];
-      load_packed_col<U>(a.G + (size_t)sc * npacked(U), l, a.kappa, acc);
-      float2 d[U];
-      bool ok;
-      const float beta = solve_sg<U>(acc, d, scr + (size_t)(lane / U) * Scr<U>::SIZE, l, a.kappa, a.coef, ok);
-      const float ib = ok ? __fdividef(1.f, beta) : 0.f;
-      whiten_sg<U, KC>(d, ib, a.s + (size_t)sc * a.K * U, a.K, lane / U, PPW, zT, l);
-      if (lane == 0) {
-        a.beta[sc] = ok ? beta : qnan();
-        if (!ok) atomicAdd(a.bad, 1);
-      }
-    }
-    __syncthreads();
-  }
-  // precode: SG g -> chunk g
-  float pw = 0.f;
-  if (sg < a.nchunks) {
-    const int g = (MODE == MODE_PRECODE && zg > 1) ? sg / a.chunks_per_zgroup : 0;
-    pw = precode_sg<U, KC>(tile, sg * a.S, a.S, zT + (size_t)g * U * zs, a.K,
-                           a.x + (size_t)sc * a.K * a.Bl + (size_t)sg * a.S, (size_t)a.Bl, l);
-  }
-  pw = sg_sum<U>(pw);
-  if (sg < a.nchunks && l == 0) a.pw[(size_t)sc * a.nchunks + sg] = pw;
 }
 
-// ================================================================== (b) standalone solve kernel
-// One SG per (subcarrier, group) problem: packed G -> beta, z = A^{-1} s / beta.
-// 4 warps per CTA.
-template <int U>
+// ================================================================== (b) solve kernel
+// One SG per (subcarrier, group) problem: packed G -> +kappa -> LDL^H -> A^{-1}
+// -> beta -> z = A^{-1} s / beta (written as z[p][k][u]).  4 warps per CTA.
+template <int U, int KC>
 __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
@@ -528,25 +651,66 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   const bool active = pr < nprob;
   const int p = active ? pr : nprob - 1;
   const int sc = p / a.groups;
-  float2 *scr = smem + (size_t)sg * Scr<U>::SIZE;
-  float2 acc[U];
-  load_packed_col<U>(a.G + (size_t)p * npacked(U), l, a.kappa, acc);
-  float2 d[U];
+  const int zs = ZL<KC>::zs(a.K);
+  constexpr int NP = npacked(U);
+  float2 *slot = smem + (size_t)sg * solve_scr_size<U, KC>(a.K);
+  float2 *Gs = slot + U, *ss = Gs + NP, *zT = ss + a.K * U;
+  sg_copy_async<U>(Gs, a.G + (size_t)p * NP, NP, l);
+  sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
+  cp_async_wait_all();
+  __syncwarp();
+  float2 col[U];
+  load_packed_col<U>(Gs, l, a.kappa, col);
   bool ok;
-  const float beta = solve_sg<U>(acc, d, scr, l, a.kappa, a.coef, ok);
-  const float ib = ok ? __fdividef(1.f, beta) : 0.f;
+  const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+  const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
+  __syncwarp();
+  whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  __syncwarp();
   if (!active) return;
-  const float2 *s = a.s + (size_t)sc * a.K * U;
-  for (int k = 0; k < a.K; ++k) {
-    float2 z = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int v = 0; v < U; ++v) cfma_cj(z, d[v], __ldg(s + (size_t)k * U + v));
-    a.zout[((size_t)p * a.K + k) * U + l] = make_float2(z.x * ib, z.y * ib);
-  }
+  float2 *zo = a.zout + (size_t)p * a.K * U;
+  for (int k = 0; k < a.K; ++k) zo[(size_t)k * U + l] = zT[ZL<KC>::idx(zs, l, k)];
   if (l == 0) {
     a.beta[p] = ok ? beta : qnan();
     if (!ok) atomicAdd(a.bad, 1);
   }
+}
+
+// ================================================================== (c) precode kernel
+// One CTA per subcarrier; SG g precodes chunk g with the z of its z group:
+// x_c = H_c^H z plus the power partial of the chunk.
+// smem: [tile Bl*U][zT zgroups*U*zs]
+template <int U, int KC>
+__global__ void __launch_bounds__(256) precode_kernel(Args a) {
+  constexpr int PPW = 32 / U;
+  extern __shared__ __align__(16) float2 smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sg = warp * PPW + lane / U, l = lane % U;
+  const int sc = blockIdx.x;
+  const int zs = ZL<KC>::zs(a.K);
+  const int zg = a.zgroups;
+  float2 *tile = smem;
+  float2 *zT = tile + (size_t)a.Bl * U;
+  load_tile_async<U>(tile, a.H + (size_t)sc * a.Bl * U, a.Bl, threadIdx.x, blockDim.x);
+  {
+    const float2 *src = a.zin + (size_t)sc * zg * a.K * U;     // z[sc][g][k][u] -> zT[g]
+    const int kend = ZL<KC>::nkc(a.K) * KC;
+    for (int i = threadIdx.x; i < zg * U * kend; i += blockDim.x) {
+      const int g = i / (U * kend), r = i % (U * kend), k = r / U, u = r % U;
+      zT[(size_t)g * U * zs + ZL<KC>::idx(zs, u, k)] =
+          (k < a.K) ? src[((size_t)g * a.K + k) * U + u] : make_float2(0.f, 0.f);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  float pw = 0.f;
+  if (sg < a.nchunks) {
+    const int g = (zg > 1) ? sg / a.chunks_per_zgroup : 0;
+    pw = precode_sg<U, KC>(tile, sg * a.S, a.S, zT + (size_t)g * U * zs, a.K,
+                           a.x + (size_t)sc * a.K * a.Bl + (size_t)sg * a.S, (size_t)a.Bl, l);
+  }
+  pw = sg_sum<U>(pw);
+  if (sg < a.nchunks && l == 0) a.pw[(size_t)sc * a.nchunks + sg] = pw;
 }
 
 // ================================================================== scalar finish
