@@ -121,14 +121,12 @@ typedef struct {
                                (check of the power constraint, Eq. 2)                     */
 
 /* kernels reported by dp_profile_read (index into its arrays) */
-#define DP_KERNEL_FUSED_FD      0   /* single pass: Gram+solve+whiten+precode, one warp-group per cluster */
-#define DP_KERNEL_FUSED_PD      1   /* single pass PD (world == 1): Gram over all antennas ... precode    */
-#define DP_KERNEL_GRAM          2   /* (a) batched Gram, packed Hermitian output                          */
-#define DP_KERNEL_SOLVE         3   /* (b) regularise + Cholesky + substitution + beta + whiten z         */
-#define DP_KERNEL_PRECODE       4   /* (c) x_c = H_c^H z + power partials                                 */
-#define DP_KERNEL_SOLVE_PRECODE 5   /* (b)+(c) in one pass over H_local (PD, world > 1, allreduce)        */
-#define DP_KERNEL_FINISH        6   /* per-subcarrier scalar combination                                  */
-#define DP_NUM_KERNELS          7
+#define DP_KERNEL_FUSED_FD      0   /* FD single pass: Gram + solve + whiten + precode per cluster     */
+#define DP_KERNEL_GRAM          1   /* (a) batched Gram, packed Hermitian output                        */
+#define DP_KERNEL_SOLVE         2   /* (b) regularise + Cholesky-type sweep + beta + whiten z           */
+#define DP_KERNEL_PRECODE       3   /* (c) x_c = H_c^H z + power partials + per-subcarrier scalars      */
+#define DP_KERNEL_FINISH        4   /* FD per-subcarrier scalar combination                             */
+#define DP_NUM_KERNELS          5
 
 /* Fill `out128` with a fresh ncclUniqueId (call on rank 0 only, then share the
  * 128 bytes with every rank, e.g. through torch.distributed). */

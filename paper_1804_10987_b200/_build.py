@@ -54,13 +54,21 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libdp.so; `out`/`defines` build experiment variants (e.g. -DDP_VARIANT=1)."""
+    if out is not None:
+        global LIB
+        saved, LIB = LIB, out
+        try:
+            return build(force=True, verbose=verbose, defines=defines)
+        finally:
+            LIB = saved
     if not force and not stale():
         return LIB
     inc, lib = nccl_dirs()
     libname = os.path.basename(sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0])
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-DDP_BUILD",
+           "-Xcompiler", "-fvisibility=hidden", "-DDP_BUILD", *[f"-D{d}" for d in defines],
            "-I", INCLUDE, "-I", CSRC, "-I", inc,
            *SOURCES, "-o", LIB + ".tmp",
            "-L", lib, f"-l:{libname}", "-Xlinker", f"-rpath,{lib}"]
@@ -73,4 +81,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
+    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, out=outs[0] if outs else None,
+          defines=defs)

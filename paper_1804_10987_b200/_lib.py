@@ -10,13 +10,13 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdp.so")
+LIB_PATH = os.environ.get("DP_LIB_PATH") or os.path.join(_HERE, "libdp.so")   # override: A/B experiments
 
 DP_OK, DP_ERR_NUMERIC, DP_ERR_INVALID, DP_ERR_CUDA, DP_ERR_NCCL, DP_ERR_UNSUPPORTED = range(6)
 DP_FLAG_SYNC, DP_FLAG_UNFUSED, DP_FLAG_PROFILE, DP_FLAG_FORCE_COMM = 1, 2, 4, 8
 DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST = 0, 1
 DP_SCALAR_BETA, DP_SCALAR_RX, DP_SCALAR_POWER = 0, 1, 2
-KERNEL_NAMES = ["fused_fd", "fused_pd", "gram", "solve", "precode", "solve_precode", "finish"]
+KERNEL_NAMES = ["fused_fd", "gram", "solve", "precode", "finish"]
 DP_NUM_KERNELS = len(KERNEL_NAMES)
 
 # every symbol include/dp.h declares (checked by tests/test_abi.py)

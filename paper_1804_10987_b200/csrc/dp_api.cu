@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -200,6 +201,24 @@ int drain_profile(dp_ctx *c) {
 // ---------------------------------------------------------------- kernel launchers
 using dpk::Args;
 
+// Launch with programmatic dependent launch (PDL): the kernel may be scheduled while
+// its predecessor on the stream drains; every kernel starts with griddepcontrol.wait.
+template <typename Kern>
+cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const Args &a) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  static const bool use_pdl = getenv("DP_NO_PDL") == nullptr;
+  cfg.attrs = attr;
+  cfg.numAttrs = use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 template <int U, int KC>
 int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int nw = c->fd_nw;
@@ -209,8 +228,7 @@ int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   auto kern = dpk::fd_fused_kernel<U, KC>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
-  kern<<<(nprob + nsg - 1) / nsg, nw * 32, sm, st>>>(a);
-  CK(cudaGetLastError());
+  CK(launch_pdl(kern, dim3((nprob + nsg - 1) / nsg), dim3(nw * 32), sm, st, a));
   return DP_OK;
 }
 
@@ -221,8 +239,7 @@ int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   auto kern = dpk::gram_kernel<U, PER_CHUNK>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_GRAM, st);
-  kern<<<a.n_sc, nw * 32, sm, st>>>(a);
-  CK(cudaGetLastError());
+  CK(launch_pdl(kern, dim3(a.n_sc), dim3(nw * 32), sm, st, a));
   return DP_OK;
 }
 
@@ -234,8 +251,7 @@ int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
   auto kern = dpk::solve_kernel<U, KC>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_SOLVE, st);
-  kern<<<(nprob + per - 1) / per, 128, sm, st>>>(a);
-  CK(cudaGetLastError());
+  CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(128), sm, st, a));
   return DP_OK;
 }
 
@@ -246,16 +262,7 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   auto kern = dpk::precode_kernel<U, KC>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
-  kern<<<a.n_sc, nw * 32, sm, st>>>(a);
-  CK(cudaGetLastError());
-  return DP_OK;
-}
-
-int launch_finish(dp_ctx *c, const float *beta, int nbeta, const float *pw, int npw, int fd,
-                  cudaStream_t st) {
-  LaunchScope ls(c, DP_KERNEL_FINISH, st);
-  dpk::finish_kernel<<<(c->cfg.n_sc + 127) / 128, 128, 0, st>>>(beta, nbeta, pw, npw, c->cfg.n_sc, fd, c->fin);
-  CK(cudaGetLastError());
+  CK(launch_pdl(kern, dim3(a.n_sc), dim3(nw * 32), sm, st, a));
   return DP_OK;
 }
 
@@ -332,6 +339,8 @@ Args base_args(dp_ctx *c) {
   a.beta = c->beta;
   a.pw = c->pw;
   a.bad = c->bad;
+  a.fin = c->fin;
+  a.fin_inv_beta = 1;
   return a;
 }
 
@@ -524,6 +533,7 @@ int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   a.nchunks = c->Cl;
   a.kappa = (float)(k.tau * k.U * N0 / rho_c2);
   a.coef = (float)(k.Es / rho_c2);
+  a.nbeta = c->Cl;
   if (k.flags & DP_FLAG_UNFUSED) {
     // (a) per-cluster Grams -> (b) solve+whiten per cluster -> (c) precode
     a.Gout = c->G;
@@ -538,8 +548,9 @@ int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
     RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
   } else {
     RET(dispatch<FdFused>(k.U, k.K, c, a, st));
+    LaunchScope ls(c, DP_KERNEL_FINISH, st);
+    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
   }
-  RET(launch_finish(c, c->beta, c->Cl, c->pw, c->Cl, 1, st));
   if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
   c->last_mode = 1;
   return finish_call(c, host, x, st);
@@ -564,6 +575,8 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   a.kappa = (float)(k.U * N0 / rho2);
   a.coef = (float)(k.Es / rho2);
   a.groups = 1;
+  a.nbeta = 1;
+  a.fin_inv_beta = (k.rank == 0) ? 1 : 0;   // 1/beta contributed once to the scalar allreduce
   const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
   const float2 *s_use = sd;
   if (!topo_t1) RET(distribute_s(c, sd, st, &s_use));   // T2: overlaps nothing yet; only s crosses
@@ -595,15 +608,8 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   a.zgroups = 1;
   a.chunks_per_zgroup = c->pd_nchunks;
   RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
-  // per-subcarrier scalars: 1/beta contributed once (rank 0), power summed over ranks
-  RET(launch_finish(c, c->beta, 1, c->pw, c->pd_nchunks, 0, st));
-  if (c->comm_on) {
-    if (k.rank != 0) {
-      // zero this rank's 1/beta contribution (stride-2 entries) before the sum
-      CK(cudaMemset2DAsync(c->fin, 2 * sizeof(float), 0, sizeof(float), k.n_sc, st));
-    }
-    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
-  }
+  // per-subcarrier scalars (written by the precode kernel): power summed over ranks
+  if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
   c->last_mode = 0;
   return finish_call(c, host, x, st);
 }

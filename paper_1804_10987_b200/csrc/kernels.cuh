@@ -510,7 +510,25 @@ struct Args {
   int zgroups;          // z groups per subcarrier in precode (1 = shared by all chunks)
   int chunks_per_zgroup;
   float kappa, coef;    // regulariser and Es / rho_x^2
+  float *fin;           // [n_sc][2]: {sum 1/beta (PD: 1/beta, FD: over local clusters), sum power}
+  int nbeta;            // beta entries per subcarrier: PD 1, FD clusters per rank
+  int fin_inv_beta;     // 1: fin[.][0] = sum 1/beta ; 0: fin[.][0] = 0 (PD ranks != 0)
 };
+
+// Programmatic dependent launch: wait for the predecessor grid's completion (and
+// memory flush) before touching its outputs; let the successor start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// Per-subcarrier scalars in a fixed order over the local parts (read through L2:
+// other CTAs wrote them).
+__device__ __forceinline__ void finish_sc(const Args &a, int sc) {
+  float ib = 0.f, p = 0.f;
+  for (int c = 0; c < a.nbeta; ++c) ib += 1.f / __ldcg(a.beta + (size_t)sc * a.nbeta + c);
+  for (int c = 0; c < a.nchunks; ++c) p += __ldcg(a.pw + (size_t)sc * a.nchunks + c);
+  a.fin[2 * sc] = a.fin_inv_beta ? ib : 0.f;
+  a.fin[2 * sc + 1] = p;
+}
 
 // ================================================================== FD fused kernel
 // One SG per (subcarrier, cluster) problem, NSG = (blockDim/32)*(32/U) problems per
@@ -520,6 +538,7 @@ struct Args {
 // smem per SG: tile S*U + scratch max(Scr::SIZE, U*zs).
 template <int U, int KC>
 __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
+  pdl_wait();
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
   const int nw = blockDim.x >> 5;
@@ -564,6 +583,7 @@ __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
   float2 *zT = Mreg + a.K * U;
   whiten_sg<U, KC>(col, ib, Mreg, a.K, 0, 1, zT, l);
   __syncwarp();
+  pdl_trigger();
   float pw = 0.f;
   if (active)
     pw = precode_sg<U, KC>(tile, 0, a.S, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
@@ -584,6 +604,7 @@ __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
 // smem: [tile Bl*U][tree (nw/2) * 32 * (3U/4) complex]
 template <int U, bool PER_CHUNK>
 __global__ void __launch_bounds__(256) gram_kernel(Args a) {
+  pdl_wait();
   constexpr int PPW = 32 / U;
   constexpr int NE = U / 2 + U / 4;
   extern __shared__ __align__(16) float2 smem[];
@@ -599,6 +620,7 @@ __global__ void __launch_bounds__(256) gram_kernel(Args a) {
   GAcc<U> g;
   g.zero();
   if (sg < a.nchunks) gram_sg<U>(tile, sg * a.S, a.S, l, g);
+  pdl_trigger();
   if constexpr (PER_CHUNK) {
     if (sg < a.nchunks) gram_store_packed<U>(g, a.Gout + ((size_t)sc * a.nchunks + sg) * npacked(U), l);
   } else {
@@ -642,6 +664,7 @@ __global__ void __launch_bounds__(256) gram_kernel(Args a) {
 // -> beta -> z = A^{-1} s / beta (written as z[p][k][u]).  4 warps per CTA.
 template <int U, int KC>
 __global__ void __launch_bounds__(128) solve_kernel(Args a) {
+  pdl_wait();
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -666,6 +689,7 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
   __syncwarp();
   whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  pdl_trigger();
   __syncwarp();
   if (!active) return;
   float2 *zo = a.zout + (size_t)p * a.K * U;
@@ -682,6 +706,7 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
 // smem: [tile Bl*U][zT zgroups*U*zs]
 template <int U, int KC>
 __global__ void __launch_bounds__(256) precode_kernel(Args a) {
+  pdl_wait();
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -703,6 +728,7 @@ __global__ void __launch_bounds__(256) precode_kernel(Args a) {
   }
   cp_async_wait_all();
   __syncthreads();
+  pdl_trigger();
   float pw = 0.f;
   if (sg < a.nchunks) {
     const int g = (zg > 1) ? sg / a.chunks_per_zgroup : 0;
@@ -711,24 +737,18 @@ __global__ void __launch_bounds__(256) precode_kernel(Args a) {
   }
   pw = sg_sum<U>(pw);
   if (sg < a.nchunks && l == 0) a.pw[(size_t)sc * a.nchunks + sg] = pw;
+  __syncthreads();
+  if (threadIdx.x == 0) finish_sc(a, sc);
 }
 
-// ================================================================== scalar finish
-// Per subcarrier, fixed order over local parts: fin[sc] = {sum_c 1/beta_c (FD) or
-// 1/beta (PD), sum of power partials}.
-__global__ void finish_kernel(const float *beta, int nbeta, const float *pw, int npw, int n_sc, int fd,
-                              float *fin) {
+// ================================================================== FD scalar finish
+// Per subcarrier, fixed order over the local clusters: fin[sc] = {sum_c 1/beta_c,
+// sum_c power_c}.  (A separate grid: folding it into the fused kernel needs a
+// release fence per cluster, which waits for that warp's x stores and cost ~10%.)
+__global__ void __launch_bounds__(128) fd_finish_kernel(Args a) {
+  pdl_wait();
   const int sc = blockIdx.x * blockDim.x + threadIdx.x;
-  if (sc >= n_sc) return;
-  float ib = 0.f, p = 0.f;
-  if (fd) {
-    for (int c = 0; c < nbeta; ++c) ib += 1.f / beta[(size_t)sc * nbeta + c];
-  } else {
-    ib = 1.f / beta[sc];
-  }
-  for (int c = 0; c < npw; ++c) p += pw[(size_t)sc * npw + c];
-  fin[2 * sc] = ib;
-  fin[2 * sc + 1] = p;
+  if (sc < a.n_sc) finish_sc(a, sc);
 }
 
 // which: 1 -> rx = 1 / fin[.][0] ; 2 -> power = fin[.][1]
