@@ -18,6 +18,7 @@
 
 #include "dp.h"
 #include "kernels.cuh"
+#include "gram_tc.cuh"
 
 namespace {
 
@@ -69,6 +70,8 @@ struct dp_ctx {
   int fd_nw = 0;     // warps per CTA of the FD fused kernel
   int fdu_nw = 0;    // warps of the FD unfused per-subcarrier kernels (chunk = cluster)
   bool comm_on = false;
+  bool use_tc = true;        // tensor-core paths where available (env DP_NO_TC=1 disables)
+  int num_sms = 148;
   ncclComm_t comm = nullptr;
   // device workspace
   float2 *s_buf = nullptr;   // broadcast landing buffer for s
@@ -234,6 +237,22 @@ int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
 
 template <int U, bool PER_CHUNK>
 int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
+  if constexpr (U == 32) {
+    if (c->use_tc && a.S % dpk::TCG_TK == 0) {   // tensor-core (tcgen05) Gram
+      Args b = a;                                 // work item = (subcarrier, group)
+      if (!PER_CHUNK) {
+        b.S = a.Bl;                               // one group: all local antennas
+        b.nchunks = 1;
+      }
+      const int n_items = b.n_sc * b.nchunks;
+      const int grid = std::min(n_items, 2 * c->num_sms);
+      auto kern = dpk::gram_tc_kernel;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::TCG_SMEM));
+      LaunchScope ls(c, DP_KERNEL_GRAM, st);
+      CK(launch_pdl(kern, dim3(grid), dim3(dpk::TCG_THREADS), dpk::TCG_SMEM, st, b));
+      return DP_OK;
+    }
+  }
   const size_t sm = smem_gram(U, a.Bl, nw);
   if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "Gram tile needs %zu B of shared memory", sm);
   auto kern = dpk::gram_kernel<U, PER_CHUNK>;
@@ -455,6 +474,8 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   dp_ctx *c = new dp_ctx();
   c->cfg = k;
   c->comm_on = comm_on;
+  c->use_tc = getenv("DP_NO_TC") == nullptr;
+  CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, k.device));
   c->Bl = k.B / k.world;
   c->Cl = k.C / k.world;
   c->S = S;

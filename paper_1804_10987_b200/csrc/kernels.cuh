@@ -583,7 +583,6 @@ __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
   float2 *zT = Mreg + a.K * U;
   whiten_sg<U, KC>(col, ib, Mreg, a.K, 0, 1, zT, l);
   __syncwarp();
-  pdl_trigger();
   float pw = 0.f;
   if (active)
     pw = precode_sg<U, KC>(tile, 0, a.S, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
@@ -594,6 +593,7 @@ __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
     a.pw[p] = pw;
     if (!ok) atomicAdd(a.bad, 1);
   }
+  pdl_trigger();
 }
 
 // ================================================================== (a) Gram kernel
@@ -620,7 +620,6 @@ __global__ void __launch_bounds__(256) gram_kernel(Args a) {
   GAcc<U> g;
   g.zero();
   if (sg < a.nchunks) gram_sg<U>(tile, sg * a.S, a.S, l, g);
-  pdl_trigger();
   if constexpr (PER_CHUNK) {
     if (sg < a.nchunks) gram_store_packed<U>(g, a.Gout + ((size_t)sc * a.nchunks + sg) * npacked(U), l);
   } else {
@@ -689,7 +688,6 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
   __syncwarp();
   whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
-  pdl_trigger();
   __syncwarp();
   if (!active) return;
   float2 *zo = a.zout + (size_t)p * a.K * U;
@@ -698,6 +696,7 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
     a.beta[p] = ok ? beta : qnan();
     if (!ok) atomicAdd(a.bad, 1);
   }
+  pdl_trigger();
 }
 
 // ================================================================== (c) precode kernel
@@ -728,7 +727,6 @@ __global__ void __launch_bounds__(256) precode_kernel(Args a) {
   }
   cp_async_wait_all();
   __syncthreads();
-  pdl_trigger();
   float pw = 0.f;
   if (sg < a.nchunks) {
     const int g = (zg > 1) ? sg / a.chunks_per_zgroup : 0;
@@ -739,6 +737,7 @@ __global__ void __launch_bounds__(256) precode_kernel(Args a) {
   if (sg < a.nchunks && l == 0) a.pw[(size_t)sc * a.nchunks + sg] = pw;
   __syncthreads();
   if (threadIdx.x == 0) finish_sc(a, sc);
+  pdl_trigger();
 }
 
 // ================================================================== FD scalar finish

@@ -270,8 +270,8 @@ def test_step_gram(cfgid):
         for c in range(cfg.C):
             g = oracle.gram(f.H[w, c * S:(c + 1) * S])
             tot += g
-            assert rel_l2(Gc[w, c], g[iu]) <= 1e-6
-        assert rel_l2(Gs[w, 0], tot[iu]) <= 1e-6
+            assert rel_l2(Gc[w, c], g[iu]) <= 1e-5   # 3xTF32 tensor-core Gram at U=32
+        assert rel_l2(Gs[w, 0], tot[iu]) <= 1e-5
 
 
 @pytest.mark.parametrize("cfgid", [1, 2, 3, 4])
