@@ -5,6 +5,8 @@
 // exchange steps (PD: Gram reduction P:280-281 and, in the paper's topology,
 // z broadcast P:296; FD: s broadcast P:255/P:299 and a 2*n_sc scalar
 // allreduce), host-pointer staging and kernel-level profiling.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -19,6 +21,7 @@
 #include "dp.h"
 #include "kernels.cuh"
 #include "gram_tc.cuh"
+#include "precode_tc.cuh"
 
 namespace {
 
@@ -206,8 +209,8 @@ using dpk::Args;
 
 // Launch with programmatic dependent launch (PDL): the kernel may be scheduled while
 // its predecessor on the stream drains; every kernel starts with griddepcontrol.wait.
-template <typename Kern>
-cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const Args &a) {
+template <typename Kern, typename... KArgs>
+cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const KArgs &...args) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -219,7 +222,7 @@ cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream
   static const bool use_pdl = getenv("DP_NO_PDL") == nullptr;
   cfg.attrs = attr;
   cfg.numAttrs = use_pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 template <int U, int KC>
@@ -282,6 +285,51 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
   CK(launch_pdl(kern, dim3(a.n_sc), dim3(nw * 32), sm, st, a));
+  return DP_OK;
+}
+
+// 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), 128-row x
+// 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
+int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        !encode)
+      return fail(DP_ERR_CUDA, "cuTensorMapEncodeTiled not available");
+  }
+  cuuint64_t dims[2] = {64, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {64 * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)H, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DP_OK;
+}
+
+// tensor-core precode applies: U = 32, K <= 16, 128-antenna items, 32-antenna z groups
+bool precode_tc_ok(const dp_ctx *c, const Args &a) {
+  static const bool opt_in = getenv("DP_TC_PRECODE") != nullptr;   // experimental (slower than SIMT today)
+  return opt_in && c->use_tc && c->cfg.U == 32 && a.K <= 16 && a.Bl % 128 == 0 && a.S == 32 &&
+         (a.zgroups == 1 || a.zgroups == a.nchunks);
+}
+
+int launch_precode_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
+  CUtensorMap tm;
+  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm));
+  auto kern = dpk::precode_tc_kernel;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::TCP_SMEM));
+  const int n_items = a.n_sc * (a.Bl / 128);
+  LaunchScope ls(c, DP_KERNEL_PRECODE, st);
+  CK(launch_pdl(kern, dim3(std::min(n_items, c->num_sms)), dim3(dpk::TCP_THREADS), dpk::TCP_SMEM, st, tm, a));
+  return DP_OK;
+}
+
+int launch_finish(dp_ctx *c, const Args &a, cudaStream_t st) {
+  LaunchScope ls(c, DP_KERNEL_FINISH, st);
+  CK(launch_pdl(dpk::fd_finish_kernel, dim3((a.n_sc + 127) / 128), dim3(128), 0, st, a));
   return DP_OK;
 }
 
@@ -628,7 +676,12 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   a.zin = c->z;
   a.zgroups = 1;
   a.chunks_per_zgroup = c->pd_nchunks;
-  RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
+  if (precode_tc_ok(c, a)) {
+    RET(launch_precode_tc(c, a, st));                // tensor-core precode (+ scalar finish)
+    RET(launch_finish(c, a, st));
+  } else {
+    RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
+  }
   // per-subcarrier scalars (written by the precode kernel): power summed over ranks
   if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
   c->last_mode = 0;
