@@ -288,7 +288,7 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   return DP_OK;
 }
 
-// 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), 128-row x
+// 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), TCP_ROWS-row x
 // 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
 int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
@@ -300,7 +300,7 @@ int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm) {
   }
   cuuint64_t dims[2] = {64, (cuuint64_t)rows};
   cuuint64_t strides[1] = {64 * 4};
-  cuuint32_t box[2] = {32, 128};
+  cuuint32_t box[2] = {32, dpk::TCP_ROWS};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)H, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -312,7 +312,7 @@ int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm) {
 // tensor-core precode applies: U = 32, K <= 16, 128-antenna items, 32-antenna z groups
 bool precode_tc_ok(const dp_ctx *c, const Args &a) {
   static const bool opt_in = getenv("DP_TC_PRECODE") != nullptr;   // experimental (slower than SIMT today)
-  return opt_in && c->use_tc && c->cfg.U == 32 && a.K <= 16 && a.Bl % 128 == 0 && a.S == 32 &&
+  return opt_in && c->use_tc && c->cfg.U == 32 && a.K <= 16 && a.Bl % dpk::TCP_ROWS == 0 && a.S == 32 &&
          (a.zgroups == 1 || a.zgroups == a.nchunks);
 }
 
@@ -321,7 +321,7 @@ int launch_precode_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm));
   auto kern = dpk::precode_tc_kernel;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::TCP_SMEM));
-  const int n_items = a.n_sc * (a.Bl / 128);
+  const int n_items = a.n_sc * (a.Bl / dpk::TCP_ROWS);
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
   CK(launch_pdl(kern, dim3(std::min(n_items, c->num_sms)), dim3(dpk::TCP_THREADS), dpk::TCP_SMEM, st, tm, a));
   return DP_OK;
