@@ -267,13 +267,16 @@ int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
 
 template <int U, int KC>
 int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
-  const int per = 4 * (32 / U);
   const int nprob = a.n_sc * a.groups;
-  const size_t sm = smem_solve(U, a.K);
+  // few problems (PD: one per subcarrier): one warp per CTA spreads the ~9k-instruction
+  // warps evenly over the SMs (4-warp CTAs left some SMs with 50% more work)
+  const int wpc = (nprob / (32 / U) <= 16 * c->num_sms) ? 1 : 4;
+  const int per = wpc * (32 / U);
+  const size_t sm = smem_solve(U, a.K) / 4 * wpc;
   auto kern = dpk::solve_kernel<U, KC>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_SOLVE, st);
-  CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(128), sm, st, a));
+  CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(32 * wpc), sm, st, a));
   return DP_OK;
 }
 

@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sg = warp * PPW + lane / U, l = lane % U;
   const int nprob = a.n_sc * a.groups;
-  const int pr = blockIdx.x * (4 * PPW) + sg;
+  const int pr = blockIdx.x * ((int)(blockDim.x >> 5) * PPW) + sg;   // 1-4 warps per CTA
   const bool active = pr < nprob;
   const int p = active ? pr : nprob - 1;
   const int sc = p / a.groups;

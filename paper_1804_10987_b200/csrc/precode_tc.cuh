@@ -25,7 +25,7 @@
 namespace dpk {
 
 constexpr int TCP_ROWS = 64;                            // antennas per item
-constexpr int TCP_NS = 2;                               // stages
+constexpr int TCP_NS = 3;                               // stages
 constexpr int TCP_HB = TCP_ROWS * 128;                  // one TMA box: 64 rows x 128 B = 8 KB
 constexpr int TCP_ZRAW = 2 * 16 * 32 * 8;               // z rows of up to 2 groups, K <= 16: 8 KB
 constexpr int TCP_Z = 64 * 64 * 4;                      // one Z operand (64 rows x 64 K, interleaved) = 16 KB
