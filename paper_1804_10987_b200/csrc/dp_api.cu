@@ -230,7 +230,8 @@ int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int nw = c->fd_nw;
   const int nsg = nw * (32 / U);
   const int nprob = a.n_sc * a.nchunks;
-  const size_t sm = smem_fd_fused(U, a.S, a.K, nw);
+  static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
+  const size_t sm = smem_fd_fused(U, a.S, a.K, nw) + pad;
   auto kern = dpk::fd_fused_kernel<U, KC>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);

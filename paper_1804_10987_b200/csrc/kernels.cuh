@@ -24,25 +24,41 @@
 namespace dpk {
 
 // ------------------------------------------------------------------ complex helpers
+// Complex multiply-accumulates run on the packed FP32 pipe (fma.rn.f32x2 -> FFMA2,
+// sm_100a): one complex MAC = 2 FFMA2,  acc += P * y.x + Q * y.y  with P, Q derived
+// from one operand.  ptxas folds the swaps / partial negations of P, Q and the
+// broadcast of y.x, y.y into FFMA2 operand modifiers (.LO_HI, .NP, .F32), so no extra
+// instructions are issued; the FMA pipe does the same work in half the issue slots.
+__device__ __forceinline__ unsigned long long pk2(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+// d += a * b (element-wise, packed)
+__device__ __forceinline__ void fma2(float2 &d, float2 a, float2 b) {
+  unsigned long long D = pk2(d);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(D) : "l"(pk2(a)), "l"(pk2(b)));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(D));
+}
+__device__ __forceinline__ void cmac2(float2 &acc, float2 P, float2 Q, float2 y) {
+  fma2(acc, P, make_float2(y.x, y.x));
+  fma2(acc, Q, make_float2(y.y, y.y));
+}
 // acc += a * conj(b)
 __device__ __forceinline__ void cfma_bc(float2 &acc, float2 a, float2 b) {
-  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
-  acc.y = fmaf(a.y, b.x, acc.y); acc.y = fmaf(-a.x, b.y, acc.y);
+  cmac2(acc, make_float2(b.x, -b.y), make_float2(b.y, b.x), a);
 }
 // acc += conj(a) * b
 __device__ __forceinline__ void cfma_cj(float2 &acc, float2 a, float2 b) {
-  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
-  acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(-a.y, b.x, acc.y);
+  cmac2(acc, make_float2(a.x, -a.y), make_float2(a.y, a.x), b);
 }
 // acc -= conj(a) * b
 __device__ __forceinline__ void cfms_cj(float2 &acc, float2 a, float2 b) {
-  acc.x = fmaf(-a.x, b.x, acc.x); acc.x = fmaf(-a.y, b.y, acc.x);
-  acc.y = fmaf(-a.x, b.y, acc.y); acc.y = fmaf(a.y, b.x, acc.y);
+  cmac2(acc, make_float2(-b.x, -b.y), make_float2(-b.y, b.x), a);
 }
 // acc -= a * b
 __device__ __forceinline__ void cfms(float2 &acc, float2 a, float2 b) {
-  acc.x = fmaf(-a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
-  acc.y = fmaf(-a.x, b.y, acc.y); acc.y = fmaf(-a.y, b.x, acc.y);
+  cmac2(acc, make_float2(-a.x, -a.y), make_float2(a.y, -a.x), b);
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
@@ -190,6 +206,49 @@ __device__ __forceinline__ void gram_to_column(const GAcc<U> &g, float2 *M, int 
   __syncwarp();
 }
 
+// Column l of G + kappa I straight from the Hermitian-reduced registers; only the
+// lower-left block (= (top-right)^H) crosses lanes through shared memory:
+//   u <  U/2           own top[u]
+//   u >= U/2, l >= U/2 bottom-right: rows U/2 .. U/2+U/4-1 from lane l - U/2 (shuffle),
+//                      the rest own br[]
+//   u >= U/2, l <  U/2 conj(top[l] of lane u), transposed through T[U/2][U/2 + 2]
+template <int U>
+__host__ __device__ constexpr int tsz(int) { return (U / 2) * (U / 2 + 2); }
+template <int U>
+__device__ __forceinline__ void gacc_to_column(const GAcc<U> &g, float2 *T, int l, float kappa,
+                                               float2 (&a)[U]) {
+  constexpr int H2 = U / 2, Q = U / 4, TS = H2 + 2;
+  const bool hi = l >= H2;
+  if (hi) {
+#pragma unroll
+    for (int r = 0; r < H2; r += 2)
+      *reinterpret_cast<float4 *>(T + (l - H2) * TS + r) =
+          make_float4(g.top[r].x, g.top[r].y, g.top[r + 1].x, g.top[r + 1].y);
+  }
+  float2 nb[Q];
+#pragma unroll
+  for (int r = 0; r < Q; ++r) {
+    nb[r].x = __shfl_xor_sync(0xffffffffu, g.br[r].x, H2, U);
+    nb[r].y = __shfl_xor_sync(0xffffffffu, g.br[r].y, H2, U);
+  }
+  __syncwarp();
+  const int lc = l % H2;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    float2 v;
+    if (u < H2) {
+      v = g.top[u];
+    } else {
+      const int j = u - H2;
+      const float2 t = T[j * TS + lc];
+      v = hi ? ((j < Q) ? nb[j] : g.br[j - Q]) : cconj(t);
+    }
+    if (u == l) { v.x += kappa; v.y = 0.f; }
+    a[u] = v;
+  }
+  __syncwarp();
+}
+
 // Upper-triangle packed index (u <= v, row-major).
 __host__ __device__ constexpr int npacked(int U) { return U * (U + 1) / 2; }
 __device__ __forceinline__ int pidx(int U, int u, int v) { return u * U - (u * (u - 1)) / 2 + (v - u); }
@@ -228,11 +287,13 @@ template <int U> struct Scr {
   static constexpr int MS = U + 2;
   static constexpr int SIZE = U + U * MS;   // complex elements
 };
-// FD fused scratch per SG: [slot U][M region]; the M region first holds the Gram
-// columns (U x MS), then s (K x U, staged during the sweep) followed by zT.
+// FD fused scratch per SG: [slot U][T region]; the T region first holds the
+// lower-left Gram block transpose (U/2 x (U/2 + 2)), then s (K x U, staged during
+// the sweep) followed by zT.  (Reading s through L1 instead cost 8%: long-scoreboard
+// stalls in the whitening loop.)
 template <int U, int KC>
 __host__ __device__ inline int fd_scr_size(int K) {
-  const int m1 = U * (U + 2), m2 = K * U + U * ZL<KC>::zs(K);
+  const int m1 = (U / 2) * (U / 2 + 2), m2 = K * U + U * ZL<KC>::zs(K);
   return U + (m1 > m2 ? m1 : m2);
 }
 // solve kernel scratch per SG: [slot U][packed G][s K x U][zT U x zs]
@@ -416,7 +477,7 @@ __device__ __forceinline__ float sweep_sg(float2 (&w)[U], float2 *slot, int l, f
 // z_k[l] = ib * sum_v conj(d[v]) s_k[v]  (d = column l of Hermitian A^{-1}, so
 // conj(d[v]) = A^{-1}[l][v]).  Written to zT for k in [kbeg, nkc*KC) step kstep,
 // zeros for k >= K.  Two symbols per iteration for independent FMA chains.
-template <int U, int KC>
+template <int U, int KC, bool GS = false>
 __device__ __forceinline__ void whiten_sg(const float2 (&d)[U], float ib, const float2 *s,
                                           int K, int kbeg, int kstep, float2 *zT, int l) {
   const int zs = ZL<KC>::zs(K);
@@ -428,8 +489,8 @@ __device__ __forceinline__ void whiten_sg(const float2 (&d)[U], float ib, const 
     const float4 *s1 = reinterpret_cast<const float4 *>(s + (size_t)min(k2, K - 1) * U);
 #pragma unroll
     for (int c = 0; c < U / 2; ++c) {
-      const float4 v = s0[c];
-      const float4 w = s1[c];
+      const float4 v = GS ? __ldg(s0 + c) : s0[c];   // GS: s read through L1 (global)
+      const float4 w = GS ? __ldg(s1 + c) : s1[c];
       cfma_cj(a0, d[2 * c], lo2(v));
       cfma_cj(a1, d[2 * c + 1], hi2(v));
       cfma_cj(b0, d[2 * c], lo2(w));
@@ -535,7 +596,7 @@ __device__ __forceinline__ void finish_sc(const Args &a, int sc) {
 // CTA with consecutive problem ids (= consecutive antenna rows of H_local).  Single
 // pass over H: cp.async tile -> Gram -> +kappa_c -> LDL^H -> L^{-1} -> A^{-1}
 // -> beta_c -> z = A^{-1} s / beta_c -> x_c = H_c^H z -> power partial.
-// smem per SG: tile S*U + scratch max(Scr::SIZE, U*zs).
+// smem per SG: tile S*U + scratch U + max(U/2 (U/2 + 2), K*U + U*zs).
 template <int U, int KC>
 __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
   pdl_wait();
@@ -565,23 +626,22 @@ __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
   const int p = active ? p0 + sg : p0;
   if (!active) tile = smem;
   const int sc = p / a.nchunks, cl = p % a.nchunks;
-  float2 *slot = scr, *Mreg = scr + U;
+  float2 *slot = scr, *T = scr + U, *ss = scr + U, *zT = ss + a.K * U;
   float2 col[U];
   {
     GAcc<U> g;
     g.zero();
     gram_sg<U>(tile, 0, a.S, l, g);
-    gram_to_column<U, Scr<U>::MS>(g, Mreg, l, a.kappa, col);
+    gacc_to_column<U>(g, T, l, a.kappa, col);
   }
-  // stage s_k of this subcarrier into the (now free) M region while the sweep runs
-  sg_copy_async<U>(Mreg, a.s + (size_t)sc * a.K * U, a.K * U, l);
+  // stage s_k of this subcarrier into the (now free) T region while the sweep runs
+  sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
   bool ok;
   const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;   // sign folds -A^{-1}; failed problems: x = 0
   cp_async_wait_all();
   __syncwarp();
-  float2 *zT = Mreg + a.K * U;
-  whiten_sg<U, KC>(col, ib, Mreg, a.K, 0, 1, zT, l);
+  whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
   __syncwarp();
   float pw = 0.f;
   if (active)
