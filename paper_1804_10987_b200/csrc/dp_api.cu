@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "gram_tc.cuh"
 #include "precode_tc.cuh"
+#include "fd_tc.cuh"
 
 namespace {
 
@@ -294,7 +295,8 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
 
 // 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), TCP_ROWS-row x
 // 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
-int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm) {
+int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows = dpk::TCP_ROWS,
+                CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -304,10 +306,10 @@ int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm) {
   }
   cuuint64_t dims[2] = {64, (cuuint64_t)rows};
   cuuint64_t strides[1] = {64 * 4};
-  cuuint32_t box[2] = {32, dpk::TCP_ROWS};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)H, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return DP_OK;
@@ -329,6 +331,34 @@ int launch_precode_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
   CK(launch_pdl(kern, dim3(std::min(n_items, c->num_sms)), dim3(dpk::TCP_THREADS), dpk::TCP_SMEM, st, tm, a));
   return DP_OK;
+}
+
+// FD with the cluster Gram on the tensor cores: U = 32, S = 32 (fd_tc.cuh)
+bool fd_tc_ok(const dp_ctx *c, const Args &a) {
+  static const bool off = getenv("DP_NO_TC_FD") != nullptr;
+  return !off && c->use_tc && c->cfg.U == 32 && a.S == 32;
+}
+
+template <int KC>
+int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
+  CUtensorMap tm;
+  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  auto kern = dpk::fd_tc_kernel<KC>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::FDT_SMEM));
+  const int nprob = a.n_sc * a.nchunks;
+  Args b = a;
+  b.pf_dist = 3 * c->num_sms;                                // resident CTAs: 3 per SM
+  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
+  CK(launch_pdl(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), dpk::FDT_SMEM, st, tm, b));
+  return DP_OK;
+}
+int launch_fd_tc_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
+  switch (kc_of(a.K)) {
+    case 7: return launch_fd_tc<7>(c, a, st);
+    case 8: return launch_fd_tc<8>(c, a, st);
+    case 14: return launch_fd_tc<14>(c, a, st);
+    default: return launch_fd_tc<16>(c, a, st);
+  }
 }
 
 int launch_finish(dp_ctx *c, const Args &a, cudaStream_t st) {
@@ -620,7 +650,8 @@ int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
     a.chunks_per_zgroup = 1;
     RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
   } else {
-    RET(dispatch<FdFused>(k.U, k.K, c, a, st));
+    if (fd_tc_ok(c, a)) RET(launch_fd_tc_kc(c, a, st));
+    else RET(dispatch<FdFused>(k.U, k.K, c, a, st));
     LaunchScope ls(c, DP_KERNEL_FINISH, st);
     CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
   }
@@ -783,7 +814,8 @@ int dp_debug_gram(dp_ctx *c, const dp_c32 *H, int per_cluster, dp_c32 *G, void *
   if (per_cluster) {
     a.S = c->S;
     a.nchunks = c->Cl;
-    RET(dispatch<GramPer>(c->cfg.U, c->cfg.K, c, a, c->fdu_nw, st));
+    if (fd_tc_ok(c, a)) RET(launch_fd_tc_kc(c, a, st));   // the FD path's own (tensor-core) Gram
+    else RET(dispatch<GramPer>(c->cfg.U, c->cfg.K, c, a, c->fdu_nw, st));
   } else {
     a.S = c->pd_chunk;
     a.nchunks = c->pd_nchunks;

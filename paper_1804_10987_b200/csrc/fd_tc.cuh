@@ -1,0 +1,282 @@
+// fd_tc.cuh — FD-WF fused kernel for U = 32, S = B_c = 32 with the cluster Gram on
+// the tensor cores (tcgen05 / TMEM / TMA, sm_100a) and the rest on the packed FP32
+// pipe.  Same per-problem math and output as fd_fused_kernel (kernels.cuh):
+//     G_c = H_c H_c^H  ->  A = G_c + kappa_c I  ->  -A^{-1}, beta_c (Lemma 1,
+//     Sec. III-C)  ->  z = A^{-1} s / beta_c  ->  x_c = H_c^H z,  power partial.
+//
+// Gram on the tensor core.  With X = the fp32 tile viewed as 32 antenna rows x 64
+// reals (j = 2u + {0: re, 1: im}),  P = X^T X  (64 x 64) and
+//     Re G[u][v] = P[2u][2v] + P[2u+1][2v+1],   Im G[u][v] = P[2u+1][2v] - P[2u][2v+1].
+// The TMA tile (two boxes of 32 reals x 32 rows, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B:
+// 32-byte chunk c of 128-byte row r stored at c ^ (r % 4)) is directly an MN-major
+// UMMA operand for both A = X^T and B = X (K = antennas) -- MN-major tf32 operands
+// must use this SWIZZLE_128B_BASE32B layout (descriptor type 1; LBO = 4096 between
+// the two 32-real atoms, SBO = 512 between 4-row K groups; verified by
+// scripts/tc_probe.py).  The raw fp32 tile is the "big" tf32 operand (the tensor
+// core reads the top 19 bits); one elementwise pass makes the residual
+// Xs = X - trunc_tf32(X) in the same layout.  3xTF32:  P = Xb^T Xb + Xs^T Xb + Xb^T Xs,
+// 12 UMMAs (M = N = 64, K = 8) accumulated in TMEM: an M = 64 accumulator uses lanes
+// 0-15 of each 32-lane quarter, so problems 2g and 2g+1 share columns 64g.. (lane
+// offset 0 / 16) and one 32x32b TMEM load feeds all 32 threads in the epilogue.
+//
+// CTA = 4 warps, one (subcarrier, cluster) problem each (12 warps per SM at 168
+// registers: the SIMT solver needs them, so there is no separate producer warp).
+//   thread 0:      TMA the 4 tiles; after its own residual, wait for the others' and
+//                  issue 4 x 12 UMMAs; commit -> mma_done.
+//   warps 0-3:     residual of their own tile -> plane_ready; then (all four, TMEM lane
+//                  quarters) read P rows 16w..16w+15 of every problem, pair rows 2l and
+//                  2l+1 across lanes (shfl_xor 1) and write G column l to the owning
+//                  warp's staging; dealloc TMEM; then the SIMT solver of fd_fused_kernel
+//                  (sweep, whitening) and the precode from the swizzled tile.
+// smem: [4 tiles x 8 KB][4 regions x 9 KB][4 slots of 2 x 32 complex]; a region holds the residual
+// plane, then the G staging (32 columns x 34 complex), then s and zT.
+#pragma once
+#include "tcgen05.cuh"
+
+namespace dpk {
+
+constexpr int FDT_TILE = 8192;                 // 32 rows x 64 fp32, two SW128 boxes of 4 KB
+constexpr int FDT_REG = 9216;                  // per-warp region (1024-aligned)
+constexpr int FDT_GLD = 34;                    // G staging column stride (complex), 272 B
+constexpr int FDT_THREADS = 128;
+constexpr size_t FDT_SMEM = 4 * FDT_TILE + 4 * FDT_REG + 4 * 64 * 8 + 1024;
+
+// UMMA shared-memory descriptor of an MN-major SWIZZLE_128B_BASE32B operand: 128-byte
+// rows along MN (32 tf32), 4-row K groups SBO bytes apart, MN atoms LBO bytes apart.
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128b32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
+}
+// kind::tf32, f32 accumulate, A and B MN-major
+__host__ __device__ constexpr uint32_t idesc_tf32_mn(int M, int N) {
+  return tc::idesc_tf32(M, N) | (1u << 15) | (1u << 16);
+}
+
+// 16-byte chunk c' (complex 2c', 2c'+1) of tile row r in the TMA SW128_ATOM_32B layout
+__device__ __forceinline__ float4 ld_chunk_sw128(const uint8_t *tile, int r, int cp) {
+  return *reinterpret_cast<const float4 *>(tile + ((cp >> 3) << 12) + (r << 7) + ((((cp & 7) >> 1) ^ (r & 3)) << 5) +
+                                           ((cp & 1) << 4));
+}
+
+// x[k][r] = sum_u conj(H[r][u]) z[k][u] for the lane's row r = l (S = U = 32)
+template <int KC>
+__device__ __forceinline__ float precode_sw128(const uint8_t *tile, const float2 *zT, int K, float2 *__restrict__ x,
+                                               size_t xstride, int l) {
+  constexpr int KCP = ZL<KC>::KCP;
+  const int zs = ZL<KC>::zs(K);
+  float pw = 0.f;
+  for (int k0 = 0, q = 0; k0 < K; k0 += KC, ++q) {
+    float2 acc[KC];
+#pragma unroll
+    for (int j = 0; j < KC; ++j) acc[j] = make_float2(0.f, 0.f);
+    const float2 *zq = zT + q * KCP;
+#pragma unroll 4
+    for (int c = 0; c < 16; ++c) {
+      const float4 h = ld_chunk_sw128(tile, l, c);
+      const float2 h0 = lo2(h), h1 = hi2(h);
+      const float2 *z0 = zq + (2 * c) * zs, *z1 = z0 + zs;
+#pragma unroll
+      for (int j = 0; j < KC; j += 2) {
+        if (j + 1 < KC) {
+          const float4 za = *reinterpret_cast<const float4 *>(z0 + j);
+          const float4 zb = *reinterpret_cast<const float4 *>(z1 + j);
+          cfma_cj(acc[j], h0, lo2(za));
+          cfma_cj(acc[j + 1], h0, hi2(za));
+          cfma_cj(acc[j], h1, lo2(zb));
+          cfma_cj(acc[j + 1], h1, hi2(zb));
+        } else {
+          cfma_cj(acc[j], h0, z0[j]);
+          cfma_cj(acc[j], h1, z1[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KC; ++j)
+      if (k0 + j < K) {
+        x[(size_t)(k0 + j) * xstride + l] = acc[j];
+        pw += cabs2(acc[j]);
+      }
+  }
+  return pw;
+}
+
+template <int KC>
+__global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
+  constexpr int U = 32;
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  // align by an offset (not integer casts) so the compiler keeps the shared state space: LDS, not LD
+  uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t tile_full[4], plane_ready[4], mma_done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nprob = a.n_sc * a.nchunks;
+  const int p0 = blockIdx.x * 4;
+  const int np = min(4, nprob - p0);
+  auto tile = [&](int p) { return sm + (size_t)p * FDT_TILE; };
+  auto region = [&](int p) { return sm + 4 * FDT_TILE + (size_t)p * FDT_REG; };
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) { tc::mbar_init(&tile_full[i], 1); tc::mbar_init(&plane_ready[i], 1); }
+    tc::mbar_init(&mma_done, 1);
+    tc::fence_mbar_init();
+    // H is an input of the call (no predecessor kernel writes it): its tiles are fetched
+    // before griddepcontrol.wait, overlapping the previous kernel's tail
+    for (int p = 0; p < np; ++p) {
+      tc::mbar_arrive_expect_tx(&tile_full[p], FDT_TILE);
+      tc::tma_load_2d(tile(p), &tmH, 0, (p0 + p) * 32, &tile_full[p]);
+      tc::tma_load_2d(tile(p) + 4096, &tmH, 32, (p0 + p) * 32, &tile_full[p]);
+    }
+    // and the tiles of the CTA that will most likely reuse this SM slot go to L2
+    const int pn = p0 + 4 * a.pf_dist;
+    if (a.pf_dist > 0 && pn < nprob) {
+      const int n = min(4, nprob - pn);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.H + (size_t)pn * 32 * U),
+                   "r"((uint32_t)n * FDT_TILE)
+                   : "memory");
+    }
+  }
+  if (warp == 0) {
+    tc::tmem_alloc(&tmem_base, 128);
+    tc::tmem_relinquish();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tm = tmem_base;
+  pdl_wait();
+
+  // ---------------------------------------------------------------- solver warps 0-3
+  const int p = warp;
+  const bool active = p < np;
+  const uint8_t *tl = tile(p);
+  uint8_t *rg = region(p);
+  if (active) {
+    tc::mbar_wait(&tile_full[p], 0);
+    const uint4 *src = reinterpret_cast<const uint4 *>(tl);
+    float4 *dst = reinterpret_cast<float4 *>(rg);
+    uint4 v16[FDT_TILE / 16 / 32];
+#pragma unroll
+    for (int j = 0; j < FDT_TILE / 16 / 32; ++j) v16[j] = src[lane + 32 * j];
+#pragma unroll
+    for (int j = 0; j < FDT_TILE / 16 / 32; ++j) {         // residual Xs = X - trunc_tf32(X)
+      const uint4 v = v16[j];
+      dst[lane + 32 * j] = make_float4(__uint_as_float(v.x) - __uint_as_float(v.x & 0xFFFFE000u),
+                           __uint_as_float(v.y) - __uint_as_float(v.y & 0xFFFFE000u),
+                           __uint_as_float(v.z) - __uint_as_float(v.z & 0xFFFFE000u),
+                           __uint_as_float(v.w) - __uint_as_float(v.w & 0xFFFFE000u));
+    }
+    tc::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&plane_ready[p]);
+  }
+  if (tid == 0) {                                             // UMMA issue (elected thread of warp 0)
+    constexpr uint32_t IDESC = idesc_tf32_mn(64, 64);
+    for (int q = 0; q < np; ++q) {
+      tc::mbar_wait(&plane_ready[q], 0);
+      tc::fence_after_sync();
+      const uint32_t xb = tc::smem_u32(tile(q)), xs = tc::smem_u32(region(q));
+      const uint32_t d = tm + 64 * (q >> 1) + ((uint32_t)(16 * (q & 1)) << 16);   // M = 64 D: lanes 16 (q&1) + 0..15
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {                            // antennas 8t .. 8t+7
+        const uint64_t b = smem_desc_mn_sw128b32(xb + 1024 * t, 4096, 512);
+        const uint64_t s = smem_desc_mn_sw128b32(xs + 1024 * t, 4096, 512);
+        tc::mma_tf32(d, b, b, IDESC, t > 0 ? 1u : 0u);         // Xb^T Xb
+        tc::mma_tf32(d, s, b, IDESC, 1u);                      // Xs^T Xb
+        tc::mma_tf32(d, b, s, IDESC, 1u);                      // Xb^T Xs
+      }
+    }
+    tc::mma_commit(&mma_done);
+  }
+  __syncwarp();
+  tc::mbar_wait(&mma_done, 0);
+  tc::fence_after_sync();
+  // ---- epilogue: TMEM lane 32 warp + i holds P row r = 16 warp + (i & 15) of problem
+  // 2 g + (i >> 4) in columns 64 g .. 64 g + 63 (two M = 64 accumulators share columns)
+  {
+    const bool odd = lane & 1;
+    const int l = (16 * warp + (lane & 15)) >> 1;             // G column produced by this lane pair
+#pragma unroll 1
+    for (int g = 0; 2 * g < np; ++g) {
+      const int q = 2 * g + (lane >> 4);
+      float2 *gst = reinterpret_cast<float2 *>(region(q < np ? q : 0));
+      const uint32_t ta = tm + 64 * g + ((uint32_t)(32 * warp) << 16);
+      float v[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tc::tmem_ld16_nowait(ta + 16 * c, v[c]);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const float *v0 = v[c], *v2 = v[c + 2];   // columns 16c.. (even lanes' half), 16(c+2).. (odd lanes')
+        float A[16], B[16];                                   // rows 2l and 2l+1 of the half this lane owns
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float r = __shfl_xor_sync(0xffffffffu, odd ? v0[j] : v2[j], 1);
+          A[j] = odd ? r : v0[j];
+          B[j] = odd ? v2[j] : r;
+        }
+        if (q < np) {
+          const int u0 = 8 * (c + (odd ? 2 : 0));
+          float4 *o = reinterpret_cast<float4 *>(gst + l * FDT_GLD + u0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            o[j] = make_float4(A[4 * j] + B[4 * j + 1], A[4 * j + 1] - B[4 * j],
+                               A[4 * j + 2] + B[4 * j + 3], A[4 * j + 3] - B[4 * j + 2]);
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  named_sync(1, 128);                                         // G staging complete, TMEM reads done
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tm, 128);
+  }
+  if (!active) return;
+  const int pr = p0 + p;
+  if (a.Gout) {                                               // dp_debug_gram: packed G_c of the FD path
+    const float2 *g = reinterpret_cast<const float2 *>(rg) + lane * FDT_GLD;
+    for (int u = 0; u <= lane; ++u) a.Gout[(size_t)pr * npacked(32) + pidx(32, u, lane)] = g[u];
+    return;
+  }
+  // ---------------------------------------------------------------- SIMT solver
+  const int sc = pr / a.nchunks, cl = pr % a.nchunks;
+  const int l = lane;
+  float2 *slot = reinterpret_cast<float2 *>(sm + 4 * FDT_TILE + 4 * FDT_REG) + 64 * p;
+  float2 col[U];
+  {
+    const float2 *g = reinterpret_cast<const float2 *>(rg) + l * FDT_GLD;
+#pragma unroll
+    for (int u = 0; u < U; u += 2) {
+      const float4 v = *reinterpret_cast<const float4 *>(g + u);
+      col[u] = lo2(v);
+      col[u + 1] = hi2(v);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (u == l) { col[u].x += a.kappa; col[u].y = 0.f; }
+  }
+  __syncwarp();
+  float2 *ss = reinterpret_cast<float2 *>(rg), *zT = ss + a.K * U;
+  sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
+  bool ok;
+  const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+  const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
+  cp_async_wait_all();
+  __syncwarp();
+  whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  __syncwarp();
+  float pw = precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l);
+  pw = sg_sum<U>(pw);
+  if (l == 0) {
+    a.beta[pr] = ok ? beta : qnan();
+    a.pw[pr] = pw;
+    if (!ok) atomicAdd(a.bad, 1);
+  }
+  pdl_trigger();
+}
+
+}  // namespace dpk

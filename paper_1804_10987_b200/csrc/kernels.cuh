@@ -287,19 +287,19 @@ template <int U> struct Scr {
   static constexpr int MS = U + 2;
   static constexpr int SIZE = U + U * MS;   // complex elements
 };
-// FD fused scratch per SG: [slot U][T region]; the T region first holds the
+// FD fused scratch per SG: [slot 2U][T region]; the T region first holds the
 // lower-left Gram block transpose (U/2 x (U/2 + 2)), then s (K x U, staged during
 // the sweep) followed by zT.  (Reading s through L1 instead cost 8%: long-scoreboard
 // stalls in the whitening loop.)
 template <int U, int KC>
 __host__ __device__ inline int fd_scr_size(int K) {
   const int m1 = (U / 2) * (U / 2 + 2), m2 = K * U + U * ZL<KC>::zs(K);
-  return U + (m1 > m2 ? m1 : m2);
+  return 2 * U + (m1 > m2 ? m1 : m2);
 }
-// solve kernel scratch per SG: [slot U][packed G][s K x U][zT U x zs]
+// solve kernel scratch per SG: [slot 2U][packed G][s K x U][zT U x zs]
 template <int U, int KC>
 __host__ __device__ inline int solve_scr_size(int K) {
-  return U + U * (U + 1) / 2 + K * U + U * ZL<KC>::zs(K);
+  return 2 * U + U * (U + 1) / 2 + K * U + U * ZL<KC>::zs(K);
 }
 
 // In: a[] = column l of A = G + kappa I (full Hermitian column).
@@ -385,14 +385,18 @@ __device__ __forceinline__ float solve_sg(float2 (&a)[U], float2 (&d)[U], float2
 // in the same pass, the k-th forward/back substitution step on the block already
 // eliminated, so after U pivots w holds column l of -A^{-1} (Goodnight's sweep).
 // Every lane updates every row at every pivot (no triangular lockstep waste), and
-// the pivot column is broadcast through `slot` using Hermitian symmetry: lane i
+// the pivot row is broadcast through `slot` using Hermitian symmetry: lane i
 // publishes its row-k entry a_ki = conj(a_ik).  The runtime pivot loop keeps the
 // code small (instruction-cache resident): R pivots are unrolled per iteration and
 // the register column is rotated by R rows at the end of it, so the pivot row is
 // always a compile-time register.
+// One-pivot look-ahead: at pivot k each lane first updates row k+1, publishes it
+// (the next pivot row) into the other half of the double-buffered slot and issues
+// the load + reciprocal of the next pivot, then updates the remaining rows; the
+// broadcast / reciprocal latency of pivot k+1 hides behind pivot k's FMAs.
 // In: w[] = column l of A = G + kappa I.  Out: w[] = column l of -A^{-1}; returns
 // beta (Lemma 1, Eq. 6); ok = false if a pivot is not finite and positive (A not
-// HPD) or beta's radicand is not.
+// HPD) or beta's radicand is not.  slot: 2U complex.
 template <int U>
 __device__ __forceinline__ float sweep_sg(float2 (&w)[U], float2 *slot, int l, float kappa, float coef,
                                           bool &ok) {
@@ -414,33 +418,54 @@ __device__ __forceinline__ float sweep_sg(float2 (&w)[U], float2 *slot, int l, f
     w[p + 1] = cscale(w[p + 1], r2.z * rl);
   }
   __syncwarp();
-  // ---- sweep
+  // ---- sweep.  Buffer k & 1 holds pivot k's row at rotated positions (l - kk) & (U-1).
+  slot[l] = w[0];
+  __syncwarp();
+  float id;
+  {
+    float d0 = slot[0].x;
+    const bool g0 = (d0 > 0.f) && (d0 < INFINITY);
+    ok = ok && g0;
+    id = __fdividef(1.f, g0 ? d0 : 1.f);
+  }
 #pragma unroll 1
   for (int kk = 0; kk < U; kk += R) {
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int k = kk + j;                       // pivot (register position j holds row k)
-      slot[(l - kk) & (U - 1)] = w[j];            // a_kl, stored at the rotated position of lane l
-      __syncwarp();
-      float dk = slot[j].x;                       // a_kk
-      const bool good = (dk > 0.f) && (dk < INFINITY);
-      ok = ok && good;
-      dk = good ? dk : 1.f;
-      const float id = __fdividef(1.f, dk);
+      const float2 *cur = slot + (j & 1) * U;     // R even: the parity of k is the parity of j
+      float2 *nxt = slot + ((j + 1) & 1) * U;
       const bool piv = (l == k);
       // Non-pivot lanes: a_pl -= a_pk a_kl / d.  The pivot lane's own column holds
       // a_pk, the Hermitian mirror of the broadcast conj(a_kp), so sigma = 1 - 1/d
       // turns it into a_pk / d (equal up to the rounding asymmetry of the mirrors,
       // which the unit-diagonal scaling keeps at the level of the pivots' rounding).
       const float2 sig = piv ? make_float2(1.f - id, 0.f) : cscale(w[j], id);
+      const int jn = (j + 1 < U) ? j + 1 : 0;       // register position of row k+1 (U = R: wraps, unused)
+      // 1. row k+1 first, published as the next pivot row
+      float idn = 1.f;
+      bool gn = true;
+      if (j + 1 < U) {
+        cfms_cj(w[jn], cur[jn], sig);
+        const int shift = (j == R - 1) ? R : 0;   // next pivot opens a new block: its base is kk + R
+        nxt[(l - kk - shift) & (U - 1)] = w[jn];
+        __syncwarp();
+        float dn = nxt[(j == R - 1) ? 0 : jn].x;  // a_{k+1,k+1}
+        gn = (dn > 0.f) && (dn < INFINITY);
+        idn = __fdividef(1.f, gn ? dn : 1.f);
+      }
+      // 2. the other rows
 #pragma unroll
       for (int p = 0; p < U; p += 2) {
-        const float4 sv = *reinterpret_cast<const float4 *>(slot + p);
-        if (p != j) cfms_cj(w[p], lo2(sv), sig);
-        if (p + 1 != j) cfms_cj(w[p + 1], hi2(sv), sig);
+        const float4 sv = *reinterpret_cast<const float4 *>(cur + p);
+        const bool done0 = (p == j) || (j + 1 < U && p == jn), done1 = (p + 1 == j) || (j + 1 < U && p + 1 == jn);
+        if (!done0) cfms_cj(w[p], lo2(sv), sig);
+        if (!done1) cfms_cj(w[p + 1], hi2(sv), sig);
       }
       w[j] = piv ? make_float2(-id, 0.f) : cscale(w[j], id);
-      __syncwarp();
+      if (k + 1 < U) ok = ok && gn;
+      id = idn;
+      __syncwarp();                               // cur is rewritten as the slot of pivot k+2
     }
     float2 t[R];                                  // rotate rows up by R
 #pragma unroll
@@ -574,6 +599,7 @@ struct Args {
   float *fin;           // [n_sc][2]: {sum 1/beta (PD: 1/beta, FD: over local clusters), sum power}
   int nbeta;            // beta entries per subcarrier: PD 1, FD clusters per rank
   int fin_inv_beta;     // 1: fin[.][0] = sum 1/beta ; 0: fin[.][0] = 0 (PD ranks != 0)
+  int pf_dist;          // fd_tc: L2-prefetch the tiles of CTA blockIdx.x + pf_dist (0: off)
 };
 
 // Programmatic dependent launch: wait for the predecessor grid's completion (and
@@ -598,7 +624,7 @@ __device__ __forceinline__ void finish_sc(const Args &a, int sc) {
 // -> beta_c -> z = A^{-1} s / beta_c -> x_c = H_c^H z -> power partial.
 // smem per SG: tile S*U + scratch U + max(U/2 (U/2 + 2), K*U + U*zs).
 template <int U, int KC>
-__global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
+__global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   pdl_wait();
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
@@ -626,7 +652,7 @@ __global__ void __launch_bounds__(128, 4) fd_fused_kernel(Args a) {
   const int p = active ? p0 + sg : p0;
   if (!active) tile = smem;
   const int sc = p / a.nchunks, cl = p % a.nchunks;
-  float2 *slot = scr, *T = scr + U, *ss = scr + U, *zT = ss + a.K * U;
+  float2 *slot = scr, *T = scr + 2 * U, *ss = scr + 2 * U, *zT = ss + a.K * U;
   float2 col[U];
   {
     GAcc<U> g;
@@ -736,7 +762,7 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   const int zs = ZL<KC>::zs(a.K);
   constexpr int NP = npacked(U);
   float2 *slot = smem + (size_t)sg * solve_scr_size<U, KC>(a.K);
-  float2 *Gs = slot + U, *ss = Gs + NP, *zT = ss + a.K * U;
+  float2 *Gs = slot + 2 * U, *ss = Gs + NP, *zT = ss + a.K * U;
   sg_copy_async<U>(Gs, a.G + (size_t)p * NP, NP, l);
   sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
   cp_async_wait_all();

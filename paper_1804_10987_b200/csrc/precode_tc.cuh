@@ -37,7 +37,8 @@ constexpr size_t TCP_SMEM = (size_t)TCP_NS * TCP_STAGE + 64 * TCP_STG_LD * 4 + 1
 __global__ void __launch_bounds__(TCP_THREADS, 1) precode_tc_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
   pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  // align by an offset (not integer casts) so the compiler keeps the shared state space: LDS, not LD
+  uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
   float *stg = reinterpret_cast<float *>(sm + (size_t)TCP_NS * TCP_STAGE);
   __shared__ __align__(8) uint64_t full[TCP_NS], prep_done[TCP_NS], stage_free[TCP_NS], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;

@@ -19,3 +19,9 @@ for w in range(n):
     print(w, f"sum relerr {e:.3e}  per-cluster max relerr {ec:.3e}")
     if w == 0:
         print("gpu", Gs[0, 0, :4], "\nref", G[iu][:4])
+G0 = oracle.gram(f.H[0, 0:32])
+Gfull = np.zeros((32, 32), complex)
+Gfull[iu] = Gc[0, 0]
+print("diag gpu", np.real(np.diag(Gfull))[:6], "\ndiag ref", np.real(np.diag(G0))[:6])
+print("row0 gpu", Gfull[0, :4], "\nrow0 ref", G0[0, :4])
+print("row20 gpu", Gfull[20, 20:24], "\nrow20 ref", G0[20, 20:24])
