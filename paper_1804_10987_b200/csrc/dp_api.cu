@@ -23,6 +23,9 @@
 #include "gram_tc.cuh"
 #include "precode_tc.cuh"
 #include "fd_tc.cuh"
+#include "solve_mw.cuh"
+#include "precode_tc2.cuh"
+#include "gram_tc2.cuh"
 
 namespace {
 
@@ -240,9 +243,32 @@ int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   return DP_OK;
 }
 
+int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw);
+
+template <int CH>
+int launch_gram_tc2(dp_ctx *c, const Args &b, cudaStream_t st) {
+  using T = dpk::GT2<CH>;
+  CUtensorMap tm;
+  RET(make_h_tmap(b.H, b.n_sc * b.Bl, &tm, CH, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  auto kern = dpk::gram_tc2_kernel<CH>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
+  LaunchScope ls(c, DP_KERNEL_GRAM, st);
+  CK(launch_pdl(kern, dim3(std::min(b.n_sc * b.nchunks, c->num_sms)), dim3(T::THREADS), T::SMEM, st, tm, b));
+  return DP_OK;
+}
+
 template <int U, bool PER_CHUNK>
 int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   if constexpr (U == 32) {
+    static const bool v1 = getenv("DP_GRAM_TC1") != nullptr;   // A/B: SIMT-built operand planes
+    if (c->use_tc && !v1 && a.S % 32 == 0) {      // tensor-core Gram, operands straight from TMA
+      Args b = a;                                 // work item = (subcarrier, group)
+      if (!PER_CHUNK) {
+        b.S = a.Bl;                               // one group: all local antennas
+        b.nchunks = 1;
+      }
+      return (b.S % 64 == 0) ? launch_gram_tc2<64>(c, b, st) : launch_gram_tc2<32>(c, b, st);
+    }
     if (c->use_tc && a.S % dpk::TCG_TK == 0) {   // tensor-core (tcgen05) Gram
       Args b = a;                                 // work item = (subcarrier, group)
       if (!PER_CHUNK) {
@@ -270,6 +296,17 @@ int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
 template <int U, int KC>
 int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int nprob = a.n_sc * a.groups;
+  if constexpr (U == 32) {
+    static const bool sg_only = getenv("DP_SOLVE_SG") != nullptr;   // A/B: one warp per problem
+    if (!sg_only) {                                                  // 4 warps per problem (solve_mw.cuh)
+      const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KC) * sizeof(float2);
+      auto kern = dpk::solve_mw_kernel<KC>;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      LaunchScope ls(c, DP_KERNEL_SOLVE, st);
+      CK(launch_pdl(kern, dim3(nprob), dim3(dpk::SMW_THREADS), sm, st, a));
+      return DP_OK;
+    }
+  }
   // few problems (PD: one per subcarrier): one warp per CTA spreads the ~9k-instruction
   // warps evenly over the SMs (4-warp CTAs left some SMs with 50% more work)
   const int wpc = (nprob / (32 / U) <= 16 * c->num_sms) ? 1 : 4;
@@ -295,8 +332,7 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
 
 // 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), TCP_ROWS-row x
 // 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
-int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows = dpk::TCP_ROWS,
-                CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -324,12 +360,29 @@ bool precode_tc_ok(const dp_ctx *c, const Args &a) {
 
 int launch_precode_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
-  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm));
+  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, dpk::TCP_ROWS, CU_TENSOR_MAP_SWIZZLE_128B));
   auto kern = dpk::precode_tc_kernel;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::TCP_SMEM));
   const int n_items = a.n_sc * (a.Bl / dpk::TCP_ROWS);
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
   CK(launch_pdl(kern, dim3(std::min(n_items, c->num_sms)), dim3(dpk::TCP_THREADS), dpk::TCP_SMEM, st, tm, a));
+  return DP_OK;
+}
+
+// PD precode on the tensor cores (precode_tc2.cuh): U = 32, one z per subcarrier,
+// K <= 16, 128-antenna blocks
+bool precode_tc2_ok(const dp_ctx *c, const Args &a) {
+  static const bool off = getenv("DP_NO_PC2") != nullptr;
+  return !off && c->use_tc && c->cfg.U == 32 && a.K <= 16 && a.Bl % dpk::PC2_ROWS == 0 && a.zgroups == 1;
+}
+
+int launch_precode_tc2(dp_ctx *c, const Args &a, cudaStream_t st) {
+  CUtensorMap tm;
+  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, dpk::PC2_ROWS, CU_TENSOR_MAP_SWIZZLE_128B));
+  auto kern = dpk::precode_tc2_kernel;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::PC2_SMEM));
+  LaunchScope ls(c, DP_KERNEL_PRECODE, st);
+  CK(launch_pdl(kern, dim3(std::min(a.n_sc, c->num_sms)), dim3(dpk::PC2_THREADS), dpk::PC2_SMEM, st, tm, a));
   return DP_OK;
 }
 
@@ -344,12 +397,14 @@ int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
   RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   auto kern = dpk::fd_tc_kernel<KC>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::FDT_SMEM));
+  static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
+  const size_t smem = dpk::FDT_SMEM + pad;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int nprob = a.n_sc * a.nchunks;
   Args b = a;
   b.pf_dist = 3 * c->num_sms;                                // resident CTAs: 3 per SM
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
-  CK(launch_pdl(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), dpk::FDT_SMEM, st, tm, b));
+  CK(launch_pdl(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), smem, st, tm, b));
   return DP_OK;
 }
 int launch_fd_tc_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
@@ -442,6 +497,8 @@ Args base_args(dp_ctx *c) {
   a.bad = c->bad;
   a.fin = c->fin;
   a.fin_inv_beta = 1;
+  static const int dbg = getenv("DP_DBG") ? atoi(getenv("DP_DBG")) : 0;
+  a.dbg = dbg;
   return a;
 }
 
@@ -711,7 +768,9 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   a.zin = c->z;
   a.zgroups = 1;
   a.chunks_per_zgroup = c->pd_nchunks;
-  if (precode_tc_ok(c, a)) {
+  if (precode_tc2_ok(c, a)) {
+    RET(launch_precode_tc2(c, a, st));               // tensor-core precode, writes the scalars
+  } else if (precode_tc_ok(c, a)) {
     RET(launch_precode_tc(c, a, st));                // tensor-core precode (+ scalar finish)
     RET(launch_finish(c, a, st));
   } else {

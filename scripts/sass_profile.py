@@ -1,7 +1,7 @@
 """Per-opcode instruction counts and stall samples of one kernel in an ncu report
 (run here, no GPU needed):
 
-    python scripts/sass_profile.py gpurun_out/x.ncu-rep [n_warps] [--runs]
+    python scripts/sass_profile.py gpurun_out/x.ncu-rep [n_warps] [--runs] [--kernel=REGEX]
 
 n_warps normalises counts to per-warp figures; --runs prints the hot straight-line
 runs (same execution count) with their stall-sample share.
@@ -16,11 +16,19 @@ import sys
 def main():
     rep = sys.argv[1]
     nw = float(sys.argv[2]) if len(sys.argv) > 2 and not sys.argv[2].startswith("-") else 1.0
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    kf = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--kernel=")]
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] +
+                         (["-k", "regex:" + kf[0]] if kf else []),
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    # with several kernels in the report only the first section is read (use --kernel=REGEX)
+    data = []
+    for r in rows[2:]:
+        if r and r[0] == "Kernel Name":
+            break
+        if len(r) == len(hdr):
+            data.append(r)
     ie, src = hdr.index("Instructions Executed"), hdr.index("Source")
     smp = hdr.index("Warp Stall Sampling (All Samples)")
     stall_cols = [c for c in hdr if c.startswith("stall_") and "Not Issued" not in c]
@@ -47,7 +55,7 @@ def main():
             else:
                 runs.append({"i": i, "len": 1, "n": n, "s": sm, "rows": [r]})
         for ru in runs:
-            if ru["s"] > 0.015 * tsamp:
+            if ru["s"] > float(next((a.split("=")[1] for a in sys.argv if a.startswith("--min=")), 0.015)) * tsamp:
                 st = collections.Counter()
                 for r in ru["rows"]:
                     for c in stall_cols:
