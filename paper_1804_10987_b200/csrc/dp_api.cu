@@ -229,6 +229,28 @@ cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// PDL launch with a thread-block cluster shape (cluster_x CTAs along x)
+template <typename Kern, typename... KArgs>
+cudaError_t launch_pdl_cluster(Kern kern, dim3 grid, dim3 block, size_t smem, int cluster_x, cudaStream_t st,
+                               const KArgs &...args) {
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cluster_x;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  static const bool use_pdl = getenv("DP_NO_PDL") == nullptr;
+  cfg.attrs = use_pdl ? attr : attr + 1;
+  cfg.numAttrs = use_pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int U, int KC>
 int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int nw = c->fd_nw;
@@ -392,6 +414,18 @@ bool fd_tc_ok(const dp_ctx *c, const Args &a) {
   return !off && c->use_tc && c->cfg.U == 32 && a.S == 32;
 }
 
+// fd_tc folds the per-subcarrier scalars into the kernel (no fd_finish_kernel) when the
+// rank's clusters of a subcarrier fill whole CTAs (Cl = 4, 8, 16, 32: a cluster of Cl/4
+// CTAs) or a CTA holds whole subcarriers (Cl = 1, 2, 4).  Returns CTAs per subcarrier, 0 = off.
+int fd_fold_of(const dp_ctx *c, const Args &a) {
+  static const bool off = getenv("DP_NO_FOLD") != nullptr;
+  if (off || a.Gout) return 0;
+  const int Cl = a.nchunks;
+  if (Cl == 4 || Cl == 8 || Cl == 16 || Cl == 32) return Cl / 4;
+  if (4 % Cl == 0) return 1;
+  return 0;
+}
+
 template <int KC>
 int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
@@ -403,8 +437,12 @@ int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int nprob = a.n_sc * a.nchunks;
   Args b = a;
   b.pf_dist = 3 * c->num_sms;                                // resident CTAs: 3 per SM
+  b.fold = fd_fold_of(c, a);
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
-  CK(launch_pdl(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), smem, st, tm, b));
+  if (b.fold > 1)
+    CK(launch_pdl_cluster(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), smem, b.fold, st, tm, b));
+  else
+    CK(launch_pdl(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), smem, st, tm, b));
   return DP_OK;
 }
 int launch_fd_tc_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
@@ -707,10 +745,13 @@ int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
     a.chunks_per_zgroup = 1;
     RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
   } else {
-    if (fd_tc_ok(c, a)) RET(launch_fd_tc_kc(c, a, st));
+    const bool tc = fd_tc_ok(c, a);
+    if (tc) RET(launch_fd_tc_kc(c, a, st));
     else RET(dispatch<FdFused>(k.U, k.K, c, a, st));
-    LaunchScope ls(c, DP_KERNEL_FINISH, st);
-    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+    if (!tc || fd_fold_of(c, a) == 0) {                       // scalars not folded into the kernel
+      LaunchScope ls(c, DP_KERNEL_FINISH, st);
+      CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+    }
   }
   if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
   c->last_mode = 1;

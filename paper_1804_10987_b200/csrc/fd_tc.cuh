@@ -105,6 +105,81 @@ __device__ __forceinline__ float precode_sw128(const uint8_t *tile, const float2
   return pw;
 }
 
+// Per-subcarrier scalars folded into the FD kernel (replaces fd_finish_kernel):
+// fin[sc] = {sum_c 1/beta_c, sum_c power_c} over the rank's Cl clusters, ascending c
+// (the order of finish_sc, so the result is bit-identical).  a.fold = CTAs per
+// subcarrier: 1 -> the CTA's 4 problems hold 4/Cl whole subcarriers; 2, 4, 8 -> a
+// thread-block cluster of a.fold CTAs (launched with that cluster shape) holds one
+// subcarrier: ranks 1.. push their 8 partials into rank 0's shared memory with
+// st.async (completion counted in bytes on rank 0's mbarrier) and exit; only rank 0
+// waits.  The mbarrier is initialised before a cluster barrier at kernel start.
+struct __align__(16) FoldSmem {
+  float rb[8][4], rp[8][4];  // rank 0: partials pushed by ranks 1..7 (16-byte rows: st.async.v4)
+  float fb[4], fp[4];        // this CTA's per-problem 1/beta_c and power
+  uint64_t bar;
+};
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(const void *p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tc::smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void fd_fold_init(const Args &a, FoldSmem &f) {
+  if (a.fold > 1) {
+    if (threadIdx.x == 0 && cluster_rank() == 0) {
+      tc::mbar_init(&f.bar, 1);
+      tc::fence_mbar_init();
+      tc::mbar_arrive_expect_tx(&f.bar, 32u * (a.fold - 1));
+    }
+    cluster_sync_all();
+  }
+}
+__device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p0, int warp, int lane, float ib, float pw) {
+  if (lane == 0) { f.fb[warp] = ib; f.fp[warp] = pw; }
+  __syncthreads();
+  const int nprob = a.n_sc * a.nchunks;
+  if (a.fold == 1) {
+    const int per = 4 / a.nchunks;                             // subcarriers in this CTA
+    if (threadIdx.x < per) {
+      const int q0 = threadIdx.x * a.nchunks, sc = (p0 + q0) / a.nchunks;
+      if (p0 + q0 < nprob) {
+        float b = 0.f, w = 0.f;
+        for (int c = 0; c < a.nchunks; ++c) { b += f.fb[q0 + c]; w += f.fp[q0 + c]; }
+        a.fin[2 * sc] = a.fin_inv_beta ? b : 0.f;
+        a.fin[2 * sc + 1] = w;
+      }
+    }
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  const uint32_t rank = cluster_rank();
+  if (rank != 0) {                                             // push to rank 0 and leave
+    st_async_v4(map_rank(&f.rb[rank][0], 0), make_float4(f.fb[0], f.fb[1], f.fb[2], f.fb[3]), map_rank(&f.bar, 0));
+    st_async_v4(map_rank(&f.rp[rank][0], 0), make_float4(f.fp[0], f.fp[1], f.fp[2], f.fp[3]), map_rank(&f.bar, 0));
+    return;
+  }
+  tc::mbar_wait(&f.bar, 0);
+  float b = 0.f, w = 0.f;
+  for (int c = 0; c < 4; ++c) { b += f.fb[c]; w += f.fp[c]; }
+  for (int r = 1; r < a.fold; ++r)
+    for (int c = 0; c < 4; ++c) { b += f.rb[r][c]; w += f.rp[r][c]; }
+  const int sc = p0 / a.nchunks;
+  a.fin[2 * sc] = a.fin_inv_beta ? b : 0.f;
+  a.fin[2 * sc + 1] = w;
+}
+
 template <int KC>
 __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
   constexpr int U = 32;
@@ -113,9 +188,11 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t tile_full[4], plane_ready[4], mma_done;
   __shared__ uint32_t tmem_base;
+  __shared__ __align__(16) FoldSmem fold;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nprob = a.n_sc * a.nchunks;
   const int p0 = blockIdx.x * 4;
+  fd_fold_init(a, fold);
   const int np = min(4, nprob - p0);
   auto tile = [&](int p) { return sm + (size_t)p * FDT_TILE; };
   auto region = [&](int p) { return sm + 4 * FDT_TILE + (size_t)p * FDT_REG; };
@@ -235,12 +312,13 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     tc::fence_after_sync();
     tc::tmem_dealloc(tm, 128);
   }
-  if (!active) return;
   const int pr = p0 + p;
+  float fold_b = 0.f, fold_p = 0.f;                           // this problem's 1/beta_c and power (fold)
+  if (active) {
   if (a.Gout) {                                               // dp_debug_gram: packed G_c of the FD path
     const float2 *g = reinterpret_cast<const float2 *>(rg) + lane * FDT_GLD;
     for (int u = 0; u <= lane; ++u) a.Gout[(size_t)pr * npacked(32) + pidx(32, u, lane)] = g[u];
-    return;
+    return;                                                   // (debug launches never fold)
   }
   // ---------------------------------------------------------------- SIMT solver
   const int sc = pr / a.nchunks, cl = pr % a.nchunks;
@@ -248,16 +326,14 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   float2 *slot = reinterpret_cast<float2 *>(sm + 4 * FDT_TILE + 4 * FDT_REG) + 64 * p;
   float2 col[U];
   {
-    const float2 *g = reinterpret_cast<const float2 *>(rg) + l * FDT_GLD;
+    float2 *g = reinterpret_cast<float2 *>(rg) + l * FDT_GLD;
+    g[l] = make_float2(g[l].x + a.kappa, 0.f);                 // A = G_c + kappa_c I (own row only)
 #pragma unroll
     for (int u = 0; u < U; u += 2) {
       const float4 v = *reinterpret_cast<const float4 *>(g + u);
       col[u] = lo2(v);
       col[u + 1] = hi2(v);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (u == l) { col[u].x += a.kappa; col[u].y = 0.f; }
   }
   __syncwarp();
   float2 *ss = reinterpret_cast<float2 *>(rg), *zT = ss + a.K * U;
@@ -276,7 +352,11 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     a.pw[pr] = pw;
     if (!ok) atomicAdd(a.bad, 1);
   }
+  fold_b = 1.f / (ok ? beta : qnan());
+  fold_p = pw;
+  }  // active
   pdl_trigger();
+  if (a.fold) fd_fold_finish(a, fold, p0, warp, lane, fold_b, fold_p);
 }
 
 }  // namespace dpk

@@ -18,12 +18,12 @@
 // and x = D[:, 0:32] + D[:, 32:64] in the epilogue.
 //
 // Persistent, warp-specialised, one CTA per SM (10 warps):
-//   warp 8     TMA producer: 128-antenna blocks of H into a 4-stage ring (Hb), the
-//              subcarrier's z rows into a double buffer.  H is an input of the call,
-//              so the first blocks are fetched before griddepcontrol.wait (overlapping
-//              the solve kernel's tail); z only after it.
-//   warps 4-7  prep: Z' operand (once per subcarrier), residual plane Hs per block into
-//              a double buffer of its own (the raw ring stays as deep as smem allows).
+//   warp 8     TMA producer: 128-antenna blocks of H into a 4-stage ring (Hb).  H is an
+//              input of the call, so it is fetched without griddepcontrol.wait
+//              (overlapping the solve kernel's tail).
+//   warps 4-7  prep: Z' operand once per subcarrier into a double buffer (the z rows are
+//              prefetched into registers one subcarrier ahead), residual plane Hs per
+//              block into a double buffer of its own.
 //   warp 9     UMMA issuer: 16 UMMAs per block into a double-buffered TMEM accumulator.
 //   warps 0-3  epilogue: TMEM lane quarter -> x rows (coalesced: one antenna per lane),
 //              the subcarrier's power, and its per-subcarrier scalars (fin).
@@ -37,19 +37,17 @@ constexpr int PC2_NS = 4;                       // raw H ring stages
 constexpr int PC2_NH = 2;                       // residual (Hs) buffers
 constexpr int PC2_BOX = PC2_ROWS * 128;         // one TMA box: 128 rows x 32 fp32 = 16 KB
 constexpr int PC2_STAGE = 2 * PC2_BOX;          // Hb: 2 K-halves = 32 KB (Hs buffers: same size)
-constexpr int PC2_ZOP = 64 * 64 * 4;            // Z' operand: 64 rows (Zb 0..31, Zs 32..63) x 64 K
-constexpr int PC2_ZRAW = 16 * 32 * 8;           // z rows of one subcarrier (K <= 16)
+constexpr int PC2_ZOP = 64 * 64 * 4;            // Z' operand: 64 rows (Zb 0..31, Zs 32..63) x 64 K (x2 buffers)
 constexpr int PC2_THREADS = 320;
-constexpr size_t PC2_SMEM = (size_t)(PC2_NS + PC2_NH) * PC2_STAGE + PC2_ZOP + 2 * PC2_ZRAW + 1024;
+constexpr size_t PC2_SMEM = (size_t)(PC2_NS + PC2_NH) * PC2_STAGE + 2 * PC2_ZOP + 1024;
 
 __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
   uint8_t *hsb = sm + (size_t)PC2_NS * PC2_STAGE;   // residual buffers
-  uint8_t *zop = hsb + (size_t)PC2_NH * PC2_STAGE;
-  uint8_t *zraw = zop + PC2_ZOP;
+  uint8_t *zop = hsb + (size_t)PC2_NH * PC2_STAGE;   // Z' double buffer
   __shared__ __align__(8) uint64_t full[PC2_NS], stage_free[PC2_NS], hs_full[PC2_NH], hs_free[PC2_NH];
-  __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2], zfull[2], zraw_empty[2], zready, zfree;
+  __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2], zready[2], zfree[2];
   __shared__ uint32_t tmem_base;
   __shared__ float pw_red[4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -71,31 +69,21 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&acc_full[i], 1);
       tc::mbar_init(&acc_empty[i], 128);
-      tc::mbar_init(&zfull[i], 1);
-      tc::mbar_init(&zraw_empty[i], 128);
+      tc::mbar_init(&zready[i], 128);
+      tc::mbar_init(&zfree[i], 1);
     }
-    tc::mbar_init(&zready, 128);
-    tc::mbar_init(&zfree, 1);
     tc::fence_mbar_init();
   }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tm = tmem_base;
-  const uint32_t zbytes = (uint32_t)a.K * 32 * 8;
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int s = 0, ph = 0, g = 0;
-      for (int item = blockIdx.x, n = 0; item < n_items; item += gridDim.x, ++n) {
-        auto load_z = [&]() {
-          const int zb = n & 1;
-          if (n >= 2) tc::mbar_wait(&zraw_empty[zb], ((n >> 1) - 1) & 1);
-          tc::mbar_arrive_expect_tx(&zfull[zb], zbytes);
-          tc::bulk_g2s(zraw + (size_t)zb * PC2_ZRAW, a.zin + (size_t)item * a.K * 32, zbytes, &zfull[zb]);
-        };
-        if (n > 0) load_z();
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         for (int blk = 0; blk < nblk; ++blk, ++g) {
           if (g >= PC2_NS) tc::mbar_wait(&stage_free[s], ph ^ 1);
           uint8_t *st = sm + (size_t)s * PC2_STAGE;
@@ -105,20 +93,16 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
           tc::tma_load_2d(st + PC2_BOX, &tmH, 32, row0, &full[s]);
           if (++s == PC2_NS) { s = 0; ph ^= 1; }
         }
-        if (n == 0) {
-          pdl_wait();                              // z is the solve kernel's output
-          load_z();
-        }
       }
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ UMMA issuer
     if (lane == 0) {
       constexpr uint32_t ID64 = tc::idesc_tf32(128, 64), ID32 = tc::idesc_tf32(128, 32);
-      const uint32_t zo = tc::smem_u32(zop);
       int s = 0, ph = 0, g = 0;
       for (int item = blockIdx.x, n = 0; item < n_items; item += gridDim.x, ++n) {
-        tc::mbar_wait(&zready, n & 1);
+        const uint32_t zo = tc::smem_u32(zop + (size_t)(n & 1) * PC2_ZOP);
+        tc::mbar_wait(&zready[n & 1], (n >> 1) & 1);
         tc::fence_after_sync();
         for (int blk = 0; blk < nblk; ++blk, ++g) {
           const int b = g & 1;
@@ -141,32 +125,43 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
           tc::mma_commit(&acc_full[b]);
           if (++s == PC2_NS) { s = 0; ph ^= 1; }
         }
-        tc::mma_commit(&zfree);
+        tc::mma_commit(&zfree[n & 1]);
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ prep (warps 4-7)
     const int ptid = tid - 128;
     int s = 0, ph = 0, g = 0;
+    // z rows of the next subcarrier are prefetched into registers (thread element e = ptid + 128 i:
+    // Z' row r = e / 32, u = e % 32, symbol k = r % 16; rows r and r + 16 read the same z)
+    pdl_wait();                                       // z is the solve kernel's output
+    float2 zv[8];
+    auto load_z = [&](int item) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = ptid + 128 * i, k = (e >> 5) & 15, u = e & 31;
+        zv[i] = (item < n_items && k < a.K) ? __ldg(a.zin + ((size_t)item * a.K + k) * 32 + u) : make_float2(0.f, 0.f);
+      }
+    };
+    load_z(blockIdx.x);
     for (int item = blockIdx.x, n = 0; item < n_items; item += gridDim.x, ++n) {
       {  // Z' = [Zb ; Zs]: rows 0..15 Re-rows k, 16..31 Im-rows k (big), rows +32 small
         const int zb = n & 1;
-        if (n >= 1) tc::mbar_wait(&zfree, (n - 1) & 1);   // previous subcarrier's UMMAs done with zop
-        tc::mbar_wait(&zfull[zb], (n >> 1) & 1);
-        const float2 *zr = reinterpret_cast<const float2 *>(zraw + (size_t)zb * PC2_ZRAW);
-#pragma unroll 2
+        uint8_t *zo = zop + (size_t)zb * PC2_ZOP;
+        if (n >= 2) tc::mbar_wait(&zfree[zb], ((n >> 1) - 1) & 1);   // UMMAs of subcarrier n-2 done with it
+#pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int e = ptid + 128 * i, r = e >> 5, u = e & 31, k = r & 15;
-          const float2 v = (k < a.K) ? zr[k * 32 + u] : make_float2(0.f, 0.f);
+          const int e = ptid + 128 * i, r = e >> 5, u = e & 31;
+          const float2 v = zv[i];
           const float c0 = (r < 16) ? v.x : v.y, c1 = (r < 16) ? v.y : -v.x;
           const uint32_t b0 = tc::to_tf32(c0), b1 = tc::to_tf32(c1);
           const uint32_t s0 = tc::to_tf32(c0 - __uint_as_float(b0)), s1 = tc::to_tf32(c1 - __uint_as_float(b1));
-          *reinterpret_cast<uint2 *>(zop + tc::kmaj_off(64, r, 2 * u)) = make_uint2(b0, b1);
-          *reinterpret_cast<uint2 *>(zop + tc::kmaj_off(64, 32 + r, 2 * u)) = make_uint2(s0, s1);
+          *reinterpret_cast<uint2 *>(zo + tc::kmaj_off(64, r, 2 * u)) = make_uint2(b0, b1);
+          *reinterpret_cast<uint2 *>(zo + tc::kmaj_off(64, 32 + r, 2 * u)) = make_uint2(s0, s1);
         }
         tc::fence_proxy_async();
-        mbar_arrive(&zraw_empty[zb]);
-        mbar_arrive(&zready);
+        mbar_arrive(&zready[zb]);
+        load_z(item + gridDim.x);
       }
       for (int blk = 0; blk < nblk; ++blk, ++g) {
         const int hbuf = g & 1;

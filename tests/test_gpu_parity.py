@@ -224,6 +224,25 @@ def test_host_pointer_path_matches_device_path(pinned):
     assert np.array_equal(xh_pd.numpy(), xd_pd) and np.array_equal(xh_fd.numpy(), xd_fd)
 
 
+@pytest.mark.parametrize("C", [1, 2, 4, 8])
+def test_fd_u32_cluster_counts(C):
+    """U = 32, S = 32 (tensor-core FD kernel) for every way the per-subcarrier scalars
+    are formed: inside one CTA (C = 1, 2, 4) and across a 2-CTA cluster (C = 8); x,
+    beta_c, the receive scale and the power vs the oracle."""
+    base = CONFIGS[4]
+    cfg = type(base)(base.cfg_id, f"u32c{C}", 13, 32 * C, 32, C, 14, 64)
+    f = frame(cfg)
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    x, beta, rx, pw, nbad = run(cfg, f, "fd", N0)
+    xr, br, rxr = reference(cfg, f, "fd", N0)
+    assert nbad == 0
+    assert rel_l2(x, xr) <= REL_TOL, rel_l2(x, xr)
+    assert np.max(np.abs(beta.reshape(br.shape) / br - 1)) <= REL_TOL
+    assert np.max(np.abs(rx / rxr - 1)) <= REL_TOL
+    pwr = np.sum(np.abs(xr) ** 2, axis=(1, 2))
+    assert np.max(np.abs(pw / pwr - 1)) <= 1e-4
+
+
 def test_fd_single_cluster_tau1_equals_pd():
     """FD with C=1, tau=1 is centralized WF, so it must equal PD (C=1)."""
     base = CONFIGS[3]
