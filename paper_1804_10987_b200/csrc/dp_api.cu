@@ -411,7 +411,7 @@ int launch_precode_tc2(dp_ctx *c, const Args &a, cudaStream_t st) {
 // FD with the cluster Gram on the tensor cores: U = 32, S = 32 (fd_tc.cuh)
 bool fd_tc_ok(const dp_ctx *c, const Args &a) {
   static const bool off = getenv("DP_NO_TC_FD") != nullptr;
-  return !off && c->use_tc && c->cfg.U == 32 && a.S == 32;
+  return !off && c->use_tc && c->cfg.U == 32 && a.S == 32 && a.K <= 16;
 }
 
 // fd_tc folds the per-subcarrier scalars into the kernel (no fd_finish_kernel) when the

@@ -63,12 +63,42 @@ __device__ __forceinline__ float4 ld_chunk_sw128(const uint8_t *tile, int r, int
                                            ((cp & 1) << 4));
 }
 
+// Whitening with the symbols innermost (K <= 16, one chunk of KC):
+//   z_k[l] = ib * sum_v conj(d[v]) s_k[v],  d = column l of -A^{-1} (Hermitian), ib = -1/beta,
+// for all k at once: per v one conj(d[v]) multiplier feeds KC independent accumulators
+// (no long dependent FMA chains), s read from a transposed copy sT[v][k] (row stride
+// FDT_SP complex, broadcast loads).  z is written as zT[u][k] (row stride FDT_SP).
+constexpr int FDT_SP = 18;    // sT / zT row stride (complex): 144 B rows, 16-byte aligned, spread banks
+template <int KC>
+__device__ __forceinline__ void whiten_T(const float2 (&d)[32], float ib, const float2 *sT, float2 *zT, int K, int l) {
+  constexpr int KP = (KC + 1) & ~1;
+  float2 acc[KP];
+#pragma unroll
+  for (int j = 0; j < KP; ++j) acc[j] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int v = 0; v < 32; ++v) {
+    const float4 *row = reinterpret_cast<const float4 *>(sT + v * FDT_SP);
+#pragma unroll
+    for (int j = 0; j < KP; j += 2) {
+      const float4 sv = row[j >> 1];
+      cfma_cj(acc[j], d[v], lo2(sv));
+      cfma_cj(acc[j + 1], d[v], hi2(sv));
+    }
+  }
+  float4 *zo = reinterpret_cast<float4 *>(zT + l * FDT_SP);
+#pragma unroll
+  for (int j = 0; j < KP; j += 2) {
+    const float a0 = j < K ? ib : 0.f, a1 = j + 1 < K ? ib : 0.f;
+    zo[j >> 1] = make_float4(acc[j].x * a0, acc[j].y * a0, acc[j + 1].x * a1, acc[j + 1].y * a1);
+  }
+}
+
 // x[k][r] = sum_u conj(H[r][u]) z[k][u] for the lane's row r = l (S = U = 32)
 template <int KC>
 __device__ __forceinline__ float precode_sw128(const uint8_t *tile, const float2 *zT, int K, float2 *__restrict__ x,
-                                               size_t xstride, int l) {
+                                               size_t xstride, int l, int zs_ = 0) {
   constexpr int KCP = ZL<KC>::KCP;
-  const int zs = ZL<KC>::zs(K);
+  const int zs = zs_ ? zs_ : ZL<KC>::zs(K);
   float pw = 0.f;
   for (int k0 = 0, q = 0; k0 < K; k0 += KC, ++q) {
     float2 acc[KC];
@@ -325,9 +355,11 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   const int l = lane;
   float2 *slot = reinterpret_cast<float2 *>(sm + 4 * FDT_TILE + 4 * FDT_REG) + 64 * p;
   float2 col[U];
+  float dl;
   {
     float2 *g = reinterpret_cast<float2 *>(rg) + l * FDT_GLD;
-    g[l] = make_float2(g[l].x + a.kappa, 0.f);                 // A = G_c + kappa_c I (own row only)
+    dl = g[l].x + a.kappa;
+    g[l] = make_float2(dl, 0.f);                                // A = G_c + kappa_c I (own row only)
 #pragma unroll
     for (int u = 0; u < U; u += 2) {
       const float4 v = *reinterpret_cast<const float4 *>(g + u);
@@ -336,16 +368,28 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     }
   }
   __syncwarp();
-  float2 *ss = reinterpret_cast<float2 *>(rg), *zT = ss + a.K * U;
+  // region: [ss (K x U), later zT (U x FDT_SP)] [sT (U x FDT_SP)]
+  float2 *ss = reinterpret_cast<float2 *>(rg), *zT = ss, *sT = ss + U * FDT_SP;
   sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
   bool ok;
-  const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+  const float beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
   cp_async_wait_all();
   __syncwarp();
-  whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  {                                                             // sT[v][k] = s_k[v] (lane v), zero padded
+    constexpr int KP = (KC + 1) & ~1;
+    float4 *row = reinterpret_cast<float4 *>(sT + l * FDT_SP);
+#pragma unroll
+    for (int j = 0; j < KP; j += 2) {
+      const float2 s0 = j < a.K ? ss[j * U + l] : make_float2(0.f, 0.f);
+      const float2 s1 = j + 1 < a.K ? ss[(j + 1) * U + l] : make_float2(0.f, 0.f);
+      row[j >> 1] = make_float4(s0.x, s0.y, s1.x, s1.y);
+    }
+  }
   __syncwarp();
-  float pw = precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l);
+  whiten_T<KC>(col, ib, sT, zT, a.K, l);
+  __syncwarp();
+  float pw = precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l, FDT_SP);
   pw = sg_sum<U>(pw);
   if (l == 0) {
     a.beta[pr] = ok ? beta : qnan();

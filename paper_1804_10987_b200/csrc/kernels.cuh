@@ -498,6 +498,99 @@ __device__ __forceinline__ float sweep_sg(float2 (&w)[U], float2 *slot, int l, f
   return good ? sqrtf(r) : 1.f;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// sweep_sg with a leaner pivot step (used by fd_tc): the caller passes its diagonal
+// entry dl = A[l][l]; reciprocals are rcp.approx.ftz (no denormal fix-up: equilibrated
+// pivots lie in (0, 1]); the per-pivot validity test is replaced by running min / max
+// of the pivots, checked once at the end (a NaN anywhere reaches tr A^{-1} and fails
+// the radicand test).  Same arithmetic on every matrix entry as sweep_sg.
+template <int U>
+__device__ __forceinline__ float sweep_sg2(float2 (&w)[U], float2 *slot, int l, float dl, float kappa, float coef,
+                                           bool &ok) {
+  constexpr int R = U >= 4 ? 4 : U;
+  const bool gd = (dl > 0.f) && (dl < INFINITY);
+  const float rl = gd ? rsqrtf(dl) : 1.f;
+  slot[l] = make_float2(rl, 0.f);
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < U; p += 2) {
+    const float4 r2 = *reinterpret_cast<const float4 *>(slot + p);
+    w[p] = cscale(w[p], r2.x * rl);
+    w[p + 1] = cscale(w[p + 1], r2.z * rl);
+  }
+  __syncwarp();
+  slot[l] = w[0];
+  __syncwarp();
+  float pmin = slot[0].x, pmax = pmin;
+  float id = rcp_approx(pmin);
+#pragma unroll 1
+  for (int kk = 0; kk < U; kk += R) {
+    const int rot = (l - kk) & (U - 1), rotn = (l - kk - R) & (U - 1);
+    const bool last_blk = kk + R >= U;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int k = kk + j;
+      const float2 *cur = slot + (j & 1) * U;
+      float2 *nxt = slot + ((j + 1) & 1) * U;
+      const bool piv = (l == k);
+      const float2 sig = piv ? make_float2(1.f - id, 0.f) : cscale(w[j], id);
+      const int jn = (j + 1 < U) ? j + 1 : 0;
+      float idn = 1.f;
+      if (j + 1 < U) {
+        cfms_cj(w[jn], cur[jn], sig);
+        nxt[(j == R - 1) ? rotn : rot] = w[jn];
+        __syncwarp();
+        float dn = nxt[(j == R - 1) ? 0 : jn].x;
+        if (j == R - 1) dn = last_blk ? 1.f : dn;   // no pivot after the last one
+        pmin = fminf(pmin, dn);
+        pmax = fmaxf(pmax, dn);
+        idn = rcp_approx(dn);
+      }
+#pragma unroll
+      for (int p = 0; p < U; p += 2) {
+        const float4 sv = *reinterpret_cast<const float4 *>(cur + p);
+        const bool done0 = (p == j) || (j + 1 < U && p == jn), done1 = (p + 1 == j) || (j + 1 < U && p + 1 == jn);
+        if (!done0) cfms_cj(w[p], lo2(sv), sig);
+        if (!done1) cfms_cj(w[p + 1], hi2(sv), sig);
+      }
+      w[j] = piv ? make_float2(-id, 0.f) : cscale(w[j], id);
+      id = idn;
+      __syncwarp();
+    }
+    float2 t[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) t[q] = w[q];
+#pragma unroll
+    for (int p = 0; p + R < U; ++p) w[p] = w[p + R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) w[U - R + q] = t[q];
+  }
+  slot[l] = make_float2(rl, 0.f);
+  __syncwarp();
+  float tr = 0.f, f = 0.f;
+#pragma unroll
+  for (int p = 0; p < U; p += 2) {
+    const float4 r2 = *reinterpret_cast<const float4 *>(slot + p);
+    w[p] = cscale(w[p], r2.x * rl);
+    w[p + 1] = cscale(w[p + 1], r2.z * rl);
+    f += cabs2(w[p]) + cabs2(w[p + 1]);
+    if (p == l) tr = -w[p].x;
+    if (p + 1 == l) tr = -w[p + 1].x;
+  }
+  __syncwarp();
+  tr = sg_sum<U>(tr);
+  f = sg_sum<U>(f);
+  // Lemma 1, Eq. (6):  beta^2 = Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)
+  const float r = coef * (tr - kappa * f);
+  ok = __all_sync(0xffffffffu, gd) && (pmin > 0.f) && (pmax < INFINITY) && (r > 0.f) && (r < INFINITY);
+  return ok ? sqrtf(r) : 1.f;
+}
+
 // ------------------------------------------------------------------ whitening
 // z_k[l] = ib * sum_v conj(d[v]) s_k[v]  (d = column l of Hermitian A^{-1}, so
 // conj(d[v]) = A^{-1}[l][v]).  Written to zT for k in [kbeg, nkc*KC) step kstep,
