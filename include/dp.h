@@ -189,6 +189,33 @@ DP_API int dp_debug_gram(dp_ctx *ctx, const dp_c32 *H_local, int per_cluster, dp
 DP_API int dp_debug_solve(dp_ctx *ctx, const dp_c32 *G_packed, int groups, const dp_c32 *s,
                    double kappa, double rho_x2, float *beta, dp_c32 *z, void *stream);
 
+/* --------------------------------------------------------------------------
+ * Uncoded-BER harness (Sec. IV-D "Simulation Results", P:236-242,
+ * Fig. 2).  Not part of the precoder: draws the paper's synthetic frames on the
+ * device and scores precoded outputs at the UEs.  Device pointers, asynchronous
+ * on `stream`; DP_ERR_INVALID for NULL pointers, dims <= 0, U > 32, B > 256,
+ * K > 16, M not in {4, 16, 64, 256}, N0 < 0.
+ *
+ * dp_synth_frame: one frame from Philox4x32-10 keyed by `seed`, counter
+ *   (index, stream, frame) — every value is a pure function of (seed, frame, index):
+ *     H     [n_sc][B][U]   i.i.d. CN(0, 1) Rayleigh (layout as H_local)
+ *     idx   [n_sc][K][U]   uniform M-QAM symbol indices (uint8), index =
+ *                          (Gray label I << log2(M)/2) | Gray label Q
+ *     s     [n_sc][K][U]   square Gray QAM points scaled to Es = 1
+ *     noise [n_sc][K][U]   i.i.d. CN(0, N0); may be NULL (not drawn)
+ * dp_receive_count: s_hat[sc][k][u] = rx[sc] (sum_b H[sc][b][u] x[sc][k][b]
+ *   + noise[sc][k][u]) — Eq. (1) with the joint UE scaling (rx from
+ *   dp_read_scalars(DP_SCALAR_RX)); per-axis nearest-level decisions; adds the
+ *   number of bit errors against idx to *errors (a device counter the caller
+ *   zeroes).  noise may be NULL (noiseless).
+ * -------------------------------------------------------------------------- */
+DP_API int dp_synth_frame(unsigned long long seed, unsigned long long frame, int n_sc, int B, int U, int K,
+                          int M, double N0, dp_c32 *H, dp_c32 *s, unsigned char *idx, dp_c32 *noise,
+                          void *stream);
+DP_API int dp_receive_count(int n_sc, int B, int U, int K, int M, const dp_c32 *H, const dp_c32 *x,
+                            const dp_c32 *noise, const float *rx, const unsigned char *idx,
+                            unsigned long long *errors, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ DP_NUM_KERNELS = len(KERNEL_NAMES)
 EXPORTS = [
     "dp_get_unique_id", "dp_init", "dp_precode_pd", "dp_precode_fd", "dp_read_scalars",
     "dp_status", "dp_profile_read", "dp_launch_count", "dp_finalize", "dp_last_error",
-    "dp_debug_gram", "dp_debug_solve",
+    "dp_debug_gram", "dp_debug_solve", "dp_synth_frame", "dp_receive_count",
 ]
 
 
@@ -67,6 +67,9 @@ def lib() -> ctypes.CDLL:
     L.dp_last_error.restype = ctypes.c_char_p
     L.dp_debug_gram.argtypes = [P, P, I, P, P]
     L.dp_debug_solve.argtypes = [P, P, I, P, D, D, P, P, P]
+    U64 = ctypes.c_ulonglong
+    L.dp_synth_frame.argtypes = [U64, U64, I, I, I, I, I, D, P, P, P, P, P]
+    L.dp_receive_count.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in ("dp_launch_count", "dp_last_error") else I
     _lib = L
@@ -136,3 +139,13 @@ def dp_debug_gram(ctx, H_ptr: int, per_cluster: bool, G_ptr: int, stream: int) -
 def dp_debug_solve(ctx, G_ptr: int, groups: int, s_ptr: int, kappa: float, rho_x2: float,
                    beta_ptr: int, z_ptr: int, stream: int) -> int:
     return lib().dp_debug_solve(ctx, G_ptr, groups, s_ptr, float(kappa), float(rho_x2), beta_ptr, z_ptr, stream)
+
+
+def dp_synth_frame(seed: int, frame: int, n_sc: int, B: int, U: int, K: int, M: int, N0: float,
+                   H_ptr: int, s_ptr: int, idx_ptr: int, noise_ptr: int, stream: int) -> int:
+    return lib().dp_synth_frame(seed, frame, n_sc, B, U, K, M, float(N0), H_ptr, s_ptr, idx_ptr, noise_ptr, stream)
+
+
+def dp_receive_count(n_sc: int, B: int, U: int, K: int, M: int, H_ptr: int, x_ptr: int, noise_ptr: int,
+                     rx_ptr: int, idx_ptr: int, errors_ptr: int, stream: int) -> int:
+    return lib().dp_receive_count(n_sc, B, U, K, M, H_ptr, x_ptr, noise_ptr, rx_ptr, idx_ptr, errors_ptr, stream)

@@ -1,0 +1,62 @@
+"""Uncoded BER sweep on the GPU (BASELINE.json configs[4] / SURVEY.md §8 f1; Fig. 2).
+
+    python scripts/ber_sweep.py [--frames F] [--snr -5:25:1] [--B 128] [--U 16] [--C 1,2,4,8] [--out PATH]
+
+Config 5: B = 128, U = 16, C in {1, 2, 4, 8}, 64-QAM, 1200 subcarriers x 14 OFDM
+symbols per frame, SNR -5..25 dB; FD-WF (tau = 0.125) vs PD-WF, which equals
+centralized WF for every C and is therefore run once (C = 1).  Frames are
+drawn on the device (dp_synth_frame), precoded by libdp and scored on the device
+(dp_receive_count).  Prints one JSON line per point and writes the table to --out.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1804_10987_b200.ber import BerRun  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--frames", type=int, default=20)
+    ap.add_argument("--snr", default="-5:25:1")
+    ap.add_argument("--B", type=int, default=128)
+    ap.add_argument("--U", type=int, default=16)
+    ap.add_argument("--C", default="1,2,4,8")
+    ap.add_argument("--n_sc", type=int, default=1200)
+    ap.add_argument("--K", type=int, default=14)
+    ap.add_argument("--M", type=int, default=64)
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    lo, hi, step = (float(v) for v in args.snr.split(":"))
+    snrs = [lo + i * step for i in range(int(round((hi - lo) / step)) + 1)]
+    Cs = [int(c) for c in args.C.split(",")]
+    run = BerRun(args.n_sc, args.B, args.U, args.K, args.M)
+    rows = []
+    t0 = time.time()
+    for snr in snrs:
+        for mode, C in [("pd", 1)] + [("fd", c) for c in Cs]:
+            e, bits = run.point(mode, C, snr, args.frames)
+            row = {"mode": "WF(=PD)" if mode == "pd" else "FD", "C": C, "B": args.B, "U": args.U,
+                   "snr_db": snr, "errors": e, "bits": bits, "ber": e / bits, "frames": args.frames}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+    torch.cuda.synchronize()
+    run.close()
+    meta = {"what": "uncoded BER, Rayleigh, GPU-drawn frames (Philox), libdp precoders", "seconds": time.time() - t0,
+            "n_sc": args.n_sc, "K": args.K, "M": args.M, "tau": 0.125}
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump({"meta": meta, "rows": rows}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
