@@ -76,7 +76,7 @@ extern "C" {
 #define DP_ERR_INVALID     2   /* bad argument: NULL pointer, dims, N0 < 0, rho2 <= 0, ...      */
 #define DP_ERR_CUDA        3   /* CUDA runtime error (message in dp_last_error)                 */
 #define DP_ERR_NCCL        4   /* NCCL error                                                    */
-#define DP_ERR_UNSUPPORTED 5   /* e.g. B/C < U (FD small-cluster branch), U > 32         */
+#define DP_ERR_UNSUPPORTED 5   /* e.g. U not in {4,8,16,32}; B/C < U with B/C not in {4,8,16}  */
 
 /* dp_config.flags */
 #define DP_FLAG_SYNC        1  /* synchronize at the end of each precode call; return numeric errors */
@@ -144,10 +144,12 @@ DP_API int dp_init(const dp_config *cfg, dp_ctx **out);
 DP_API int dp_precode_pd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
                   double N0, double rho2, dp_c32 *x_local, void *stream);
 
-/* FD-WF frame (Sec. III-C): for every local cluster c,
- * x_c = H_c^H (H_c H_c^H + kappa_c I)^{-1} s / beta_c with rho_c^2 = rho2 / C,
- * kappa_c = tau U N0 / rho_c^2.  Only s (and 2 n_sc scalars) cross ranks.
- * Returns DP_ERR_UNSUPPORTED if B/C < U (branch B_c < U of P:230). */
+/* FD-WF frame (Sec. III-C): for every local cluster c, x_c = Q_c s / beta_c with
+ * rho_c^2 = rho2 / C, kappa_c = tau U N0 / rho_c^2 (Eq. 9) and
+ *   Q_c = H_c^H (H_c H_c^H + kappa_c I_U)^{-1}        if B_c >= U
+ *   Q_c = (H_c^H H_c + kappa_c I_{B_c})^{-1} H_c^H    if B_c <  U (B_c in {4, 8, 16};
+ *         defined at N0 = 0 when H_c has full column rank)
+ * beta_c^2 = Es tr(Q_c^H Q_c) / rho_c^2.  Only s (and 2 n_sc scalars) cross ranks. */
 DP_API int dp_precode_fd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
                   double N0, double rho2, dp_c32 *x_local, void *stream);
 

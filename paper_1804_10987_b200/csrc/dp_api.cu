@@ -27,6 +27,7 @@
 #include "precode_tc2.cuh"
 #include "gram_tc2.cuh"
 #include "ber.cuh"
+#include "fd_small.cuh"
 
 namespace {
 
@@ -250,6 +251,39 @@ cudaError_t launch_pdl_cluster(Kern kern, dim3 grid, dim3 block, size_t smem, in
   cfg.attrs = use_pdl ? attr : attr + 1;
   cfg.numAttrs = use_pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// FD small-cluster branch B_c = S < U (fd_small.cuh)
+template <int S, int U, int KC>
+int launch_fd_small_t(dp_ctx *c, const Args &a, cudaStream_t st) {
+  constexpr int NSG = 4 * (32 / S);                      // 4 warps per CTA
+  const size_t sm = (size_t)NSG * dpk::fds_size<S, U, KC>(a.K) * sizeof(float2);
+  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "FD small-cluster tiles need %zu B of shared memory", sm);
+  auto kern = dpk::fd_small_kernel<S, U, KC>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const int nprob = a.n_sc * a.nchunks;
+  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
+  CK(launch_pdl(kern, dim3((nprob + NSG - 1) / NSG), dim3(128), sm, st, a));
+  return DP_OK;
+}
+template <int S, int U>
+int launch_fd_small_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
+  switch (kc_of(a.K)) {
+    case 7: return launch_fd_small_t<S, U, 7>(c, a, st);
+    case 8: return launch_fd_small_t<S, U, 8>(c, a, st);
+    case 14: return launch_fd_small_t<S, U, 14>(c, a, st);
+    default: return launch_fd_small_t<S, U, 16>(c, a, st);
+  }
+}
+int launch_fd_small(dp_ctx *c, const Args &a, cudaStream_t st) {
+  const int S = a.S, U = c->cfg.U;
+  if (S == 4 && U == 8) return launch_fd_small_kc<4, 8>(c, a, st);
+  if (S == 4 && U == 16) return launch_fd_small_kc<4, 16>(c, a, st);
+  if (S == 4 && U == 32) return launch_fd_small_kc<4, 32>(c, a, st);
+  if (S == 8 && U == 16) return launch_fd_small_kc<8, 16>(c, a, st);
+  if (S == 8 && U == 32) return launch_fd_small_kc<8, 32>(c, a, st);
+  if (S == 16 && U == 32) return launch_fd_small_kc<16, 32>(c, a, st);
+  return fail(DP_ERR_UNSUPPORTED, "FD small-cluster branch: B_c=%d, U=%d (need B_c in {4, 8, 16} < U)", S, U);
 }
 
 template <int U, int KC>
@@ -644,7 +678,8 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   if (k.U != 4 && k.U != 8 && k.U != 16 && k.U != 32)
     return fail(DP_ERR_UNSUPPORTED, "U=%d: supported U are 4, 8, 16, 32", k.U);
   const int S = k.B / k.C;
-  if (S < k.U) return fail(DP_ERR_UNSUPPORTED, "B/C=%d < U=%d (FD branch B_c < U, P:230, not implemented)", S, k.U);
+  if (S < k.U && S != 4 && S != 8 && S != 16)   // FD branch B_c < U: fd_small.cuh
+    return fail(DP_ERR_UNSUPPORTED, "B/C=%d < U=%d: the small-cluster branch supports B_c in {4, 8, 16}", S, k.U);
   const bool comm_on = k.world > 1 || (k.flags & DP_FLAG_FORCE_COMM);
   if (comm_on && !k.nccl_id) return fail(DP_ERR_INVALID, "nccl_id is required when world > 1 or DP_FLAG_FORCE_COMM");
 
@@ -660,6 +695,11 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   // per-subcarrier PD kernels: split clusters into chunks (>= U rows) until the
   // CTA has >= 256 threads of SGs
   int chunk = S;
+  if (S < k.U) {                        // small clusters: PD chunks span several clusters (>= U rows)
+    chunk = c->Bl;
+    for (int m = S; m < c->Bl; m += S)
+      if (m >= k.U && c->Bl % m == 0) { chunk = m; break; }
+  }
   while ((c->Bl / chunk) * k.U < 256 && chunk % 16 == 0 && chunk / 2 >= k.U) chunk /= 2;
   c->pd_chunk = chunk;
   c->pd_nchunks = c->Bl / chunk;
@@ -733,7 +773,12 @@ int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   a.kappa = (float)(k.tau * k.U * N0 / rho_c2);
   a.coef = (float)(k.Es / rho_c2);
   a.nbeta = c->Cl;
-  if (k.flags & DP_FLAG_UNFUSED) {
+  if (c->S < k.U) {
+    // small clusters (B_c < U): B_c x B_c regularised Gram per cluster
+    RET(launch_fd_small(c, a, st));
+    LaunchScope ls(c, DP_KERNEL_FINISH, st);
+    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+  } else if (k.flags & DP_FLAG_UNFUSED) {
     // (a) per-cluster Grams -> (b) solve+whiten per cluster -> (c) precode
     a.Gout = c->G;
     RET(dispatch<GramPer>(k.U, k.K, c, a, c->fdu_nw, st));

@@ -1,6 +1,6 @@
 """Uncoded BER sweep on the GPU (BASELINE.json configs[4] / SURVEY.md §8 f1; Fig. 2).
 
-    python scripts/ber_sweep.py [--frames F] [--snr -5:25:1] [--B 128] [--U 16] [--C 1,2,4,8] [--out PATH]
+    python scripts/ber_sweep.py [--frames F] [--snr=-5:25:1] [--B 128] [--U 16] [--C 1,2,4,8] [--out PATH]
 
 Config 5: B = 128, U = 16, C in {1, 2, 4, 8}, 64-QAM, 1200 subcarriers x 14 OFDM
 symbols per frame, SNR -5..25 dB; FD-WF (tau = 0.125) vs PD-WF, which equals

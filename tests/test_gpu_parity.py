@@ -243,6 +243,40 @@ def test_fd_u32_cluster_counts(C):
     assert np.max(np.abs(pw / pwr - 1)) <= 1e-4
 
 
+@pytest.mark.parametrize("S,U", [(4, 8), (8, 16), (4, 16), (16, 32), (8, 32)])
+@pytest.mark.parametrize("mode", ["pd", "fd"])
+def test_small_clusters_bc_below_u(S, U, mode):
+    """B_c = S < U: FD takes the B_c x B_c branch Q_c = (H_c^H H_c + kappa_c I)^{-1} H_c^H
+    (fd_small.cuh); PD is unaffected by the cluster size.  The oracle's
+    FD implements that branch step by step (oracle.c)."""
+    base = CONFIGS[3]
+    C = 4
+    cfg = type(base)(base.cfg_id, f"s{S}u{U}", 21, S * C, U, C, 14, 16)
+    f = frame(cfg)
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    x, beta, rx, pw, nbad = run(cfg, f, mode, N0)
+    xr, br, rxr = reference(cfg, f, mode, N0)
+    assert nbad == 0
+    assert rel_l2(x, xr) <= REL_TOL, rel_l2(x, xr)
+    assert np.max(np.abs(beta.reshape(br.shape) / br - 1)) <= REL_TOL
+    assert np.max(np.abs(rx / rxr - 1)) <= REL_TOL
+    pwr = np.sum(np.abs(xr) ** 2, axis=(1, 2))
+    assert np.max(np.abs(pw / pwr - 1)) <= 1e-4
+
+
+def test_small_clusters_zero_noise():
+    """At N0 = 0 the B_c x B_c branch stays defined (H_c^H H_c has full rank B_c < U) where
+    the U x U form would be singular: FD precodes without numeric failures and matches the
+    oracle's zero-forcing-per-cluster result."""
+    base = CONFIGS[3]
+    cfg = type(base)(base.cfg_id, "s8u16n0", 9, 32, 16, 4, 14, 16)
+    f = frame(cfg)
+    x, beta, rx, pw, nbad = run(cfg, f, "fd", 0.0)
+    xr, br, rxr = reference(cfg, f, "fd", 0.0)
+    assert nbad == 0
+    assert rel_l2(x, xr) <= 1e-3, rel_l2(x, xr)
+
+
 def test_fd_single_cluster_tau1_equals_pd():
     """FD with C=1, tau=1 is centralized WF, so it must equal PD (C=1)."""
     base = CONFIGS[3]
