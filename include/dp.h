@@ -192,6 +192,26 @@ DP_API int dp_debug_solve(dp_ctx *ctx, const dp_c32 *G_packed, int groups, const
                    double kappa, double rho_x2, float *beta, dp_c32 *z, void *stream);
 
 /* --------------------------------------------------------------------------
+ * Prepare / apply split.  The whitening matrix depends only on
+ * the channel, so it is computed once per channel realisation and applied to
+ * every OFDM symbol (A^{-1} and beta computed once, reused for
+ * the K symbols).  Device pointers only; asynchronous on `stream`.
+ * dp_prepare_pd / dp_prepare_fd: Gram (+ cross-rank sum for PD, collective when
+ *   world > 1; every rank solves) -> A = G + kappa I -> W = A^{-1}/beta (Lemma 1),
+ *   cached in the context as packed Hermitian W per (subcarrier, group) with beta.
+ *   N0, rho2 as in dp_precode_*.  FD with B_c < U: DP_ERR_UNSUPPORTED (fused only).
+ * dp_apply: x_local = H_local^H W s for Ka in [1, K] symbols s [n_sc][Ka][U]
+ *   (z = W s, then the precode of the prepared mode); x_local [n_sc][Ka][B/world].
+ *   dp_read_scalars afterwards gives beta, rx and the power of these Ka symbols.
+ *   Equal (up to rounding order) to dp_precode_* on the same H, s, N0, rho2.
+ *   DP_ERR_INVALID without a preceding prepare; any dp_precode_* call discards
+ *   the prepared state (shared workspace).
+ * -------------------------------------------------------------------------- */
+DP_API int dp_prepare_pd(dp_ctx *ctx, const dp_c32 *H_local, double N0, double rho2, void *stream);
+DP_API int dp_prepare_fd(dp_ctx *ctx, const dp_c32 *H_local, double N0, double rho2, void *stream);
+DP_API int dp_apply(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s, int Ka, dp_c32 *x_local, void *stream);
+
+/* --------------------------------------------------------------------------
  * Uncoded-BER harness (Sec. IV-D "Simulation Results", P:236-242,
  * Fig. 2).  Not part of the precoder: draws the paper's synthetic frames on the
  * device and scores precoded outputs at the UEs.  Device pointers, asynchronous

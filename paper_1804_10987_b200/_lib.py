@@ -24,6 +24,7 @@ EXPORTS = [
     "dp_get_unique_id", "dp_init", "dp_precode_pd", "dp_precode_fd", "dp_read_scalars",
     "dp_status", "dp_profile_read", "dp_launch_count", "dp_finalize", "dp_last_error",
     "dp_debug_gram", "dp_debug_solve", "dp_synth_frame", "dp_receive_count",
+    "dp_prepare_pd", "dp_prepare_fd", "dp_apply",
 ]
 
 
@@ -67,6 +68,9 @@ def lib() -> ctypes.CDLL:
     L.dp_last_error.restype = ctypes.c_char_p
     L.dp_debug_gram.argtypes = [P, P, I, P, P]
     L.dp_debug_solve.argtypes = [P, P, I, P, D, D, P, P, P]
+    L.dp_prepare_pd.argtypes = [P, P, D, D, P]
+    L.dp_prepare_fd.argtypes = [P, P, D, D, P]
+    L.dp_apply.argtypes = [P, P, P, I, P, P]
     U64 = ctypes.c_ulonglong
     L.dp_synth_frame.argtypes = [U64, U64, I, I, I, I, I, D, P, P, P, P, P]
     L.dp_receive_count.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P]
@@ -149,3 +153,15 @@ def dp_synth_frame(seed: int, frame: int, n_sc: int, B: int, U: int, K: int, M: 
 def dp_receive_count(n_sc: int, B: int, U: int, K: int, M: int, H_ptr: int, x_ptr: int, noise_ptr: int,
                      rx_ptr: int, idx_ptr: int, errors_ptr: int, stream: int) -> int:
     return lib().dp_receive_count(n_sc, B, U, K, M, H_ptr, x_ptr, noise_ptr, rx_ptr, idx_ptr, errors_ptr, stream)
+
+
+def dp_prepare_pd(ctx, H_ptr: int, N0: float, rho2: float, stream: int) -> int:
+    return lib().dp_prepare_pd(ctx, H_ptr, float(N0), float(rho2), stream)
+
+
+def dp_prepare_fd(ctx, H_ptr: int, N0: float, rho2: float, stream: int) -> int:
+    return lib().dp_prepare_fd(ctx, H_ptr, float(N0), float(rho2), stream)
+
+
+def dp_apply(ctx, H_ptr: int, s_ptr: int, Ka: int, x_ptr: int, stream: int) -> int:
+    return lib().dp_apply(ctx, H_ptr, s_ptr, Ka, x_ptr, stream)

@@ -88,6 +88,28 @@ class Precoder:
         """FD-WF (Sec. III-C): per-cluster WF with rho_c^2 = rho^2/C, kappa_c = tau U N0/rho_c^2."""
         return self._run(L.dp_precode_fd, "dp_precode_fd", H, s, N0, rho2, out, stream)
 
+    # ------------------------------------------------------------ prepare / apply (P:286-289)
+    def prepare_pd(self, H, N0: float, rho2: float = 1.0, stream=None):
+        """Cache W = A^{-1}/beta^WF for this channel (PD); then apply() per batch of symbols."""
+        self._check_io(H, None, None)
+        L.check(L.dp_prepare_pd(self.ctx, _ptr(H), N0, rho2, self._stream(stream)), "dp_prepare_pd")
+        self._prepared = "dp_precode_pd"
+
+    def prepare_fd(self, H, N0: float, rho2: float = 1.0, stream=None):
+        """Cache W_c = A_c^{-1}/beta_c per cluster (FD); then apply() per batch of symbols."""
+        self._check_io(H, None, None)
+        L.check(L.dp_prepare_fd(self.ctx, _ptr(H), N0, rho2, self._stream(stream)), "dp_prepare_fd")
+        self._prepared = "dp_precode_fd"
+
+    def apply(self, H, s, out=None, stream=None):
+        """x_local = H_local^H W s for s [n_sc][Ka][U], 1 <= Ka <= K (the prepared mode's W)."""
+        Ka = s.shape[1] if s is not None else self.K
+        x = out if out is not None else torch.empty((self.n_sc, Ka, self.Bl), dtype=torch.complex64, device=H.device)
+        L.check(L.dp_apply(self.ctx, _ptr(H), _ptr(s) if s is not None else None, Ka, _ptr(x), self._stream(stream)),
+                "dp_apply")
+        self._last = getattr(self, "_prepared", None)
+        return x
+
     def read_scalars(self, which: str, device="cuda", stream=None) -> torch.Tensor:
         """'beta' (PD [n_sc]; FD local [n_sc][C/world]), 'rx' [n_sc], 'power' [n_sc]."""
         w = {"beta": L.DP_SCALAR_BETA, "rx": L.DP_SCALAR_RX, "power": L.DP_SCALAR_POWER}[which]

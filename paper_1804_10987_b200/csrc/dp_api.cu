@@ -95,6 +95,7 @@ struct dp_ctx {
   float2 *h_dev = nullptr, *s_dev = nullptr, *x_dev = nullptr;
   // last call
   int last_mode = -1;        // 0 pd, 1 fd
+  int prepared = -1;         // W cached in G by dp_prepare_pd (0) / dp_prepare_fd (1); -1 none
   // profiling
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
@@ -528,6 +529,20 @@ template <int U, int KC> struct GramPer {
 template <int U, int KC> struct Precode {
   static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) { return launch_precode<U, KC>(c, a, nw, st); }
 };
+template <int U, int KC>
+int launch_whiten(dp_ctx *c, const Args &a, cudaStream_t st) {
+  const int nprob = a.n_sc * a.groups;
+  const int per = 4 * (32 / U);
+  const size_t sm = (size_t)per * (dpk::npacked(U) + a.K * U + U * dpk::ZL<KC>::zs(a.K)) * sizeof(float2);
+  auto kern = dpk::whiten_kernel<U, KC>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  LaunchScope ls(c, DP_KERNEL_SOLVE, st);
+  CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(128), sm, st, a));
+  return DP_OK;
+}
+template <int U, int KC> struct Whiten {
+  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_whiten<U, KC>(c, a, st); }
+};
 template <int U, int KC> struct Solve {
   static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_solve<U, KC>(c, a, st); }
 };
@@ -613,12 +628,12 @@ int stage_out(dp_ctx *c, bool host, dp_c32 *x, cudaStream_t st) {
 }
 
 // s broadcast from rank 0 ("the vector s is the only signal that must be broadcast")
-int distribute_s(dp_ctx *c, const float2 *s, cudaStream_t st, const float2 **s_use) {
+int distribute_s(dp_ctx *c, const float2 *s, cudaStream_t st, const float2 **s_use, int K = 0) {
   if (!c->comm_on || c->cfg.s_on_all_ranks) {
     *s_use = s;
     return DP_OK;
   }
-  const size_t n = (size_t)c->cfg.n_sc * c->cfg.K * c->cfg.U * 2;
+  const size_t n = (size_t)c->cfg.n_sc * (K > 0 ? K : c->cfg.K) * c->cfg.U * 2;
   if (c->cfg.rank == 0) {
     NK(ncclBroadcast(s, (void *)s, n, ncclFloat, 0, c->comm, st));
     *s_use = s;
@@ -801,6 +816,7 @@ int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   }
   if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
   c->last_mode = 1;
+  c->prepared = -1;                                       // G workspace reused
   return finish_call(c, host, x, st);
 }
 
@@ -866,6 +882,7 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   // per-subcarrier scalars (written by the precode kernel): power summed over ranks
   if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
   c->last_mode = 0;
+  c->prepared = -1;
   return finish_call(c, host, x, st);
 }
 
@@ -984,6 +1001,121 @@ int dp_debug_solve(dp_ctx *c, const dp_c32 *G, int groups, const dp_c32 *s, doub
   a.kappa = (float)kappa;
   a.coef = (float)(c->cfg.Es / rho_x2);
   RET(dispatch<Solve>(c->cfg.U, c->cfg.K, c, a, st));
+  return DP_OK;
+}
+
+// ---------------------------------------------------------------- prepare / apply (f2)
+int dp_prepare_pd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stream) {
+  g_err.clear();
+  if (!c || !H) return fail(DP_ERR_INVALID, "ctx and H_local must be non-NULL");
+  if (!is_device_ptr(H)) return fail(DP_ERR_INVALID, "dp_prepare_pd takes device pointers");
+  if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
+  if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->cfg.device));
+  const dp_config &k = c->cfg;
+  Args a = base_args(c);
+  a.H = reinterpret_cast<const float2 *>(H);
+  a.S = c->pd_chunk;
+  a.nchunks = c->pd_nchunks;
+  a.kappa = (float)(k.U * N0 / rho2);                      // Eq. 5
+  a.coef = (float)(k.Es / rho2);
+  a.groups = 1;
+  a.nbeta = 1;
+  a.Gout = c->G;
+  RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));   // G_c summed over local clusters
+  if (c->comm_on)                                         // every rank holds sum_c G_c
+    NK(ncclAllReduce(c->G, c->G, (size_t)k.n_sc * dpk::npacked(k.U) * 2, ncclFloat, ncclSum, c->comm, st));
+  a.G = c->G;
+  a.Wout = c->G;                                          // W = A^{-1}/beta in place of G
+  a.s = nullptr;
+  RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  c->prepared = 0;
+  return DP_OK;
+}
+
+int dp_prepare_fd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stream) {
+  g_err.clear();
+  if (!c || !H) return fail(DP_ERR_INVALID, "ctx and H_local must be non-NULL");
+  if (!is_device_ptr(H)) return fail(DP_ERR_INVALID, "dp_prepare_fd takes device pointers");
+  if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
+  if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");
+  if (c->S < c->cfg.U) return fail(DP_ERR_UNSUPPORTED, "prepare/apply: FD branch B_c < U runs fused only");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->cfg.device));
+  const dp_config &k = c->cfg;
+  const double rho_c2 = rho2 / k.C;
+  Args a = base_args(c);
+  a.H = reinterpret_cast<const float2 *>(H);
+  a.S = c->S;
+  a.nchunks = c->Cl;
+  a.kappa = (float)(k.tau * k.U * N0 / rho_c2);            // Eq. 9
+  a.coef = (float)(k.Es / rho_c2);
+  a.groups = c->Cl;
+  a.nbeta = c->Cl;
+  a.Gout = c->G;
+  RET(dispatch<GramPer>(k.U, k.K, c, a, c->fdu_nw, st));  // G_c per local cluster
+  a.Gout = nullptr;
+  a.G = c->G;
+  a.Wout = c->G;
+  a.s = nullptr;
+  RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  c->prepared = 1;
+  return DP_OK;
+}
+
+int dp_apply(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, int Ka, dp_c32 *x, void *stream) {
+  g_err.clear();
+  if (!c || !H || !x) return fail(DP_ERR_INVALID, "ctx, H_local and x_local must be non-NULL");
+  if (c->prepared < 0) return fail(DP_ERR_INVALID, "no prepared channel (dp_prepare_pd / dp_prepare_fd first)");
+  if (Ka < 1 || Ka > c->cfg.K) return fail(DP_ERR_INVALID, "Ka=%d must be in [1, K=%d]", Ka, c->cfg.K);
+  const bool need_s = c->cfg.s_on_all_ranks || c->cfg.rank == 0;
+  if (need_s && !s) return fail(DP_ERR_INVALID, "s must be non-NULL on this rank");
+  if (!is_device_ptr(H) || !is_device_ptr(x) || (s && !is_device_ptr(s)))
+    return fail(DP_ERR_INVALID, "dp_apply takes device pointers");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->cfg.device));
+  const dp_config &k = c->cfg;
+  const float2 *s_use;
+  RET(distribute_s(c, reinterpret_cast<const float2 *>(s), st, &s_use, Ka));
+  const bool fd = c->prepared == 1;
+  Args a = base_args(c);
+  a.H = reinterpret_cast<const float2 *>(H);
+  a.x = reinterpret_cast<float2 *>(x);
+  a.s = s_use;
+  a.K = Ka;
+  a.G = c->G;                                             // cached W
+  a.zout = c->z;
+  a.groups = fd ? c->Cl : 1;
+  a.nbeta = fd ? c->Cl : 1;
+  a.fin_inv_beta = (fd || k.rank == 0) ? 1 : 0;
+  RET(dispatch<Whiten>(k.U, Ka, c, a, st));                // z = W s
+  a.zin = c->z;
+  if (fd) {
+    a.S = c->S;
+    a.nchunks = c->Cl;
+    a.zgroups = c->Cl;
+    a.chunks_per_zgroup = 1;
+    RET(dispatch<Precode>(k.U, Ka, c, a, c->fdu_nw, st));  // x_c = H_c^H z_c
+  } else {
+    a.S = c->pd_chunk;
+    a.nchunks = c->pd_nchunks;
+    a.zgroups = 1;
+    a.chunks_per_zgroup = c->pd_nchunks;
+    if (precode_tc2_ok(c, a)) RET(launch_precode_tc2(c, a, st));
+    else RET(dispatch<Precode>(k.U, Ka, c, a, c->pd_nw, st));
+  }
+  if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+  c->last_mode = c->prepared;
+  if (k.flags & DP_FLAG_SYNC) {
+    CK(cudaStreamSynchronize(st));
+    int nb = 0;
+    CK(cudaMemcpy(&nb, c->bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (nb > 0) {
+      CK(cudaMemset(c->bad, 0, sizeof(int)));
+      return fail(DP_ERR_NUMERIC, "%d (subcarrier, cluster) problems had a non-HPD regularised Gram", nb);
+    }
+  }
   return DP_OK;
 }
 

@@ -680,6 +680,7 @@ struct Args {
   float2 *Gout;         // packed Gram output [n_sc][groups][U(U+1)/2]  (gram kernel)
   const float2 *zin;    // z input  [n_sc][zgroups][K][U]                (precode kernel)
   float2 *zout;         // z output [n_sc][groups][K][U]                 (solve kernel)
+  float2 *Wout;         // prepare: W = A^{-1}/beta packed [n_sc][groups][U(U+1)/2] (solve kernel; no z)
   float *beta;          // per-problem beta (NaN when not HPD)
   float *pw;            // per (subcarrier, chunk) power partials [n_sc][nchunks]
   int *bad;             // count of non-HPD problems
@@ -859,7 +860,7 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   float2 *slot = smem + (size_t)sg * solve_scr_size<U, KC>(a.K);
   float2 *Gs = slot + 2 * U, *ss = Gs + NP, *zT = ss + a.K * U;
   sg_copy_async<U>(Gs, a.G + (size_t)p * NP, NP, l);
-  sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
+  if (!a.Wout) sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);   // prepare: no symbols
   cp_async_wait_all();
   __syncwarp();
   float2 col[U];
@@ -867,6 +868,19 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   bool ok;
   const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
+  if (a.Wout) {                                   // prepare: cache W = A^{-1} / beta (upper, packed)
+    if (active) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (u <= l) a.Wout[(size_t)p * NP + pidx(U, u, l)] = cscale(col[u], ib);
+      if (l == 0) {
+        a.beta[p] = ok ? beta : qnan();
+        if (!ok) atomicAdd(a.bad, 1);
+      }
+    }
+    pdl_trigger();
+    return;
+  }
   __syncwarp();
   whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
   __syncwarp();
@@ -877,6 +891,40 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
     a.beta[p] = ok ? beta : qnan();
     if (!ok) atomicAdd(a.bad, 1);
   }
+  pdl_trigger();
+}
+
+// ================================================================== apply: whitening from cached W
+// One SG per (subcarrier, group) problem: z_k = W s_k with the W = A^{-1}/beta cached by
+// a prepare call (packed Hermitian), for the a.K symbols of this apply call (P:286-289:
+// the whitening matrix is computed once per channel and applied to every symbol).
+template <int U, int KC>
+__global__ void __launch_bounds__(128) whiten_kernel(Args a) {
+  pdl_wait();
+  constexpr int PPW = 32 / U;
+  constexpr int NP = npacked(U);
+  extern __shared__ __align__(16) float2 smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sg = warp * PPW + lane / U, l = lane % U;
+  const int nprob = a.n_sc * a.groups;
+  const int pr = blockIdx.x * ((int)(blockDim.x >> 5) * PPW) + sg;
+  const bool active = pr < nprob;
+  const int p = active ? pr : nprob - 1;
+  const int sc = p / a.groups;
+  const int zs = ZL<KC>::zs(a.K);
+  float2 *Ws = smem + (size_t)sg * (NP + a.K * U + U * zs);
+  float2 *ss = Ws + NP, *zT = ss + a.K * U;
+  sg_copy_async<U>(Ws, a.G + (size_t)p * NP, NP, l);
+  sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
+  cp_async_wait_all();
+  __syncwarp();
+  float2 col[U];
+  load_packed_col<U>(Ws, l, 0.f, col);            // column l of W (Hermitian; real diagonal)
+  whiten_sg<U, KC>(col, 1.f, ss, a.K, 0, 1, zT, l);
+  __syncwarp();
+  if (!active) return;
+  float2 *zo = a.zout + (size_t)p * a.K * U;
+  for (int k = 0; k < a.K; ++k) zo[(size_t)k * U + l] = zT[ZL<KC>::idx(zs, l, k)];
   pdl_trigger();
 }
 

@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   //
   if (tid == 0) bad = 0;
   pdl_wait();
   for (int i = tid; i < NP / 2; i += SMW_THREADS) cp_async16(Gs + 2 * i, a.G + (size_t)p * NP + 2 * i);
-  for (int i = tid; i < a.K * U / 2; i += SMW_THREADS) cp_async16(ss + 2 * i, a.s + (size_t)sc * a.K * U + 2 * i);
+  if (!a.Wout)                                          // prepare calls have no symbols
+    for (int i = tid; i < a.K * U / 2; i += SMW_THREADS) cp_async16(ss + 2 * i, a.s + (size_t)sc * a.K * U + 2 * i);
   cp_async_wait_all();
   __syncthreads();
 
@@ -145,6 +146,17 @@ __global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   //
   const bool ok = (bad == 0) && (rad > 0.f) && (rad < INFINITY);
   const float beta = ok ? sqrtf(rad) : 1.f;
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;   // -: c holds -A^{-1}; failed problems: z = 0
+  if (a.Wout) {                                         // prepare: cache W = A^{-1} / beta (upper, packed)
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (R * w + r <= l) a.Wout[(size_t)p * NP + pidx(U, R * w + r, l)] = cscale(c[r], ib);
+    if (tid == 0) {
+      a.beta[p] = ok ? beta : qnan();
+      if (!ok) atomicAdd(a.bad, 1);
+    }
+    pdl_trigger();
+    return;
+  }
 
   // ---- whitening z_k[l] = (1/beta) sum_v A^{-1}[l][v] s_k[v], A^{-1}[l][v] = conj(A^{-1}[v][l])
   float2 *zo = a.zout + (size_t)p * a.K * U;

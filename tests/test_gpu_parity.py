@@ -277,6 +277,50 @@ def test_small_clusters_zero_noise():
     assert rel_l2(x, xr) <= 1e-3, rel_l2(x, xr)
 
 
+@pytest.mark.parametrize("cfgid", [2, 3, 4])
+@pytest.mark.parametrize("mode", ["pd", "fd"])
+def test_prepare_apply_matches_oracle(cfgid, mode):
+    """Prepare/apply split: W = A^{-1}/beta cached once per
+    channel, applied to symbol batches of 1, 5 and the remaining symbols; every batch's
+    x equals the oracle's frame restricted to those symbols, beta and rx are the frame's."""
+    cfg = CONFIGS[cfgid]
+    f = frame(cfg, 23)
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    xr, br, rxr = reference(cfg, f, mode, N0)
+    H = torch.from_numpy(f.H).cuda()
+    s = torch.from_numpy(f.s).cuda()
+    with Precoder(23, cfg.B, cfg.U, cfg.K, cfg.C, tau=cfg.tau) as pre:
+        (pre.prepare_pd if mode == "pd" else pre.prepare_fd)(H, N0, 1.0)
+        k0 = 0
+        for Ka in (1, 5, cfg.K - 6):
+            x = pre.apply(H, s[:, k0:k0 + Ka].contiguous())
+            beta = pre.read_scalars("beta").cpu().numpy()
+            rx = pre.read_scalars("rx").cpu().numpy()
+            pw = pre.read_scalars("power").cpu().numpy()
+            torch.cuda.synchronize()
+            xs = xr[:, k0:k0 + Ka]
+            assert rel_l2(x.cpu().numpy(), xs) <= REL_TOL, (Ka, rel_l2(x.cpu().numpy(), xs))
+            assert np.max(np.abs(beta.reshape(br.shape) / br - 1)) <= REL_TOL
+            assert np.max(np.abs(rx / rxr - 1)) <= REL_TOL
+            assert np.max(np.abs(pw / np.sum(np.abs(xs) ** 2, axis=(1, 2)) - 1)) <= 1e-4
+            k0 += Ka
+        assert pre.status() == 0
+
+
+def test_apply_without_prepare_rejected():
+    cfg = CONFIGS[2]
+    f = frame(cfg, 5)
+    H = torch.from_numpy(f.H).cuda()
+    s = torch.from_numpy(f.s).cuda()
+    with Precoder(5, cfg.B, cfg.U, cfg.K, cfg.C) as pre:
+        with pytest.raises(L.DpError):
+            pre.apply(H, s)
+        pre.prepare_pd(H, 0.1)
+        pre.precode_fd(H, s, 0.1)            # discards the prepared state
+        with pytest.raises(L.DpError):
+            pre.apply(H, s)
+
+
 def test_fd_single_cluster_tau1_equals_pd():
     """FD with C=1, tau=1 is centralized WF, so it must equal PD (C=1)."""
     base = CONFIGS[3]
