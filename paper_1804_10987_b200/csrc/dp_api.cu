@@ -462,11 +462,11 @@ int fd_fold_of(const dp_ctx *c, const Args &a) {
   return 0;
 }
 
-template <int KC>
+template <int KC, bool WTC>
 int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
   RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
-  auto kern = dpk::fd_tc_kernel<KC>;
+  auto kern = dpk::fd_tc_kernel<KC, WTC>;
   static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
   const size_t smem = dpk::FDT_SMEM + pad;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -482,11 +482,21 @@ int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   return DP_OK;
 }
 int launch_fd_tc_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
+  static const bool simt_w = getenv("DP_FD_SIMT_WHITEN") != nullptr;   // A/B: SIMT whitening
+  // tensor-core whitening stacks a CTA's 4 problems on one s: they must share the subcarrier
+  if (simt_w || a.nchunks % 4 != 0) {
+    switch (kc_of(a.K)) {
+      case 7: return launch_fd_tc<7, false>(c, a, st);
+      case 8: return launch_fd_tc<8, false>(c, a, st);
+      case 14: return launch_fd_tc<14, false>(c, a, st);
+      default: return launch_fd_tc<16, false>(c, a, st);
+    }
+  }
   switch (kc_of(a.K)) {
-    case 7: return launch_fd_tc<7>(c, a, st);
-    case 8: return launch_fd_tc<8>(c, a, st);
-    case 14: return launch_fd_tc<14>(c, a, st);
-    default: return launch_fd_tc<16>(c, a, st);
+    case 7: return launch_fd_tc<7, true>(c, a, st);
+    case 8: return launch_fd_tc<8, true>(c, a, st);
+    case 14: return launch_fd_tc<14, true>(c, a, st);
+    default: return launch_fd_tc<16, true>(c, a, st);
   }
 }
 

@@ -210,13 +210,14 @@ __device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p
   a.fin[2 * sc + 1] = w;
 }
 
-template <int KC>
+// WTC: whitening on the tensor cores (see below); false: SIMT whitening (whiten_T)
+template <int KC, bool WTC>
 __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
   constexpr int U = 32;
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   // align by an offset (not integer casts) so the compiler keeps the shared state space: LDS, not LD
   uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t tile_full[4], plane_ready[4], mma_done;
+  __shared__ __align__(8) uint64_t tile_full[4], plane_ready[4], mma_done, wz_done[2];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) FoldSmem fold;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -229,6 +230,8 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) { tc::mbar_init(&tile_full[i], 1); tc::mbar_init(&plane_ready[i], 1); }
     tc::mbar_init(&mma_done, 1);
+    tc::mbar_init(&wz_done[0], 1);
+    tc::mbar_init(&wz_done[1], 1);
     tc::fence_mbar_init();
     // H is an input of the call (no predecessor kernel writes it): its tiles are fetched
     // before griddepcontrol.wait, overlapping the previous kernel's tail
@@ -338,25 +341,32 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   }
   tc::fence_before_sync();
   named_sync(1, 128);                                         // G staging complete, TMEM reads done
-  if (warp == 0) {
+  if (!WTC && warp == 0) {
     tc::fence_after_sync();
     tc::tmem_dealloc(tm, 128);
   }
   const int pr = p0 + p;
   float fold_b = 0.f, fold_p = 0.f;                           // this problem's 1/beta_c and power (fold)
-  if (active) {
-  if (a.Gout) {                                               // dp_debug_gram: packed G_c of the FD path
+  if (active && a.Gout) {                                     // dp_debug_gram: packed G_c of the FD path
     const float2 *g = reinterpret_cast<const float2 *>(rg) + lane * FDT_GLD;
     for (int u = 0; u <= lane; ++u) a.Gout[(size_t)pr * npacked(32) + pidx(32, u, lane)] = g[u];
-    return;                                                   // (debug launches never fold)
+  }
+  if (a.Gout) {                                               // (debug launches never fold)
+    if (WTC) {
+      tc::fence_after_sync();
+      if (warp == 0) tc::tmem_dealloc(tm, 128);
+    }
+    return;
   }
   // ---------------------------------------------------------------- SIMT solver
-  const int sc = pr / a.nchunks, cl = pr % a.nchunks;
+  const int sc = (active ? pr : p0) / a.nchunks, cl = pr % a.nchunks;
   const int l = lane;
   float2 *slot = reinterpret_cast<float2 *>(sm + 4 * FDT_TILE + 4 * FDT_REG) + 64 * p;
   float2 col[U];
-  float dl;
-  {
+#pragma unroll
+  for (int u = 0; u < U; ++u) col[u] = make_float2(0.f, 0.f);
+  float dl = 1.f;
+  if (active) {
     float2 *g = reinterpret_cast<float2 *>(rg) + l * FDT_GLD;
     dl = g[l].x + a.kappa;
     g[l] = make_float2(dl, 0.f);                                // A = G_c + kappa_c I (own row only)
@@ -368,37 +378,131 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     }
   }
   __syncwarp();
-  // region: [ss (K x U), later zT (U x FDT_SP)] [sT (U x FDT_SP)]
+  // region: [ss (K x U), later zT (U x FDT_SP)] [sT (U x FDT_SP) | WTC: pieces of the s operand]
   float2 *ss = reinterpret_cast<float2 *>(rg), *zT = ss, *sT = ss + U * FDT_SP;
-  sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
-  bool ok;
-  const float beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
-  const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
-  cp_async_wait_all();
-  __syncwarp();
-  {                                                             // sT[v][k] = s_k[v] (lane v), zero padded
-    constexpr int KP = (KC + 1) & ~1;
-    float4 *row = reinterpret_cast<float4 *>(sT + l * FDT_SP);
+  auto piece = [&](int q) { return region(q >> 2) + 4608 + 1024 * (q & 3); };   // S' piece q = plane * 8 + t
+  if constexpr (WTC) {
+    // ---- Whitening on the tensor cores:  Z = A^{-1} S / beta for the CTA's 4 problems at
+    // once (they share s: same subcarrier).  Real form with j = 2v + {0: re, 1: im}:
+    //   A'[32p + u][j]  = (A_p^{-1}[u][v] / beta_p) (re, im)         M = 128 (4 x 32 rows)
+    //   S'[n][j]: n = k < 16: (Re s_k[v], -Im s_k[v]); n = 16 + k: (Im s_k[v], Re s_k[v])   N = 32
+    //   D[32p + u][k] = Re z_k[u], D[32p + u][16 + k] = Im z_k[u]     (K = 64)
+    // A' is written by each warp into its own TMEM lane quarter (A operand from TMEM),
+    // S' (K-major interleaved, N = 32) in 16 pieces of 1 KB (one per K step and plane)
+    // in the regions' second halves.  3xTF32: A'b S'b + A'b S's, then A's S'b after A's
+    // replaces A'b in TMEM (TMEM holds 128 columns: A' 64, D 32).
+    named_sync(1, 128);                                       // every warp has read its G staging
 #pragma unroll
-    for (int j = 0; j < KP; j += 2) {
-      const float2 s0 = j < a.K ? ss[j * U + l] : make_float2(0.f, 0.f);
-      const float2 s1 = j + 1 < a.K ? ss[(j + 1) * U + l] : make_float2(0.f, 0.f);
-      row[j >> 1] = make_float4(s0.x, s0.y, s1.x, s1.y);
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + 128 * i, n = e >> 5, v = e & 31, k = n & 15;
+      float2 w = make_float2(0.f, 0.f);
+      if (k < a.K) {
+        const float2 sv = __ldg(a.s + ((size_t)sc * a.K + k) * U + v);
+        w = n < 16 ? make_float2(sv.x, -sv.y) : make_float2(sv.y, sv.x);
+      }
+      const int j = 2 * v, t = j >> 3;
+      const uint32_t off = ((j & 7) >> 2) * 512 + (n >> 3) * 128 + (n & 7) * 16 + (j & 3) * 4;
+      *reinterpret_cast<float2 *>(piece(t) + off) = w;
+      const float2 r = make_float2(w.x - __uint_as_float(__float_as_uint(w.x) & 0xFFFFE000u),
+                                   w.y - __uint_as_float(__float_as_uint(w.y) & 0xFFFFE000u));
+      *reinterpret_cast<float2 *>(piece(8 + t) + off) = r;
+    }
+    tc::fence_proxy_async();
+  } else {
+    sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
+  }
+  bool ok = false;
+  float beta = 1.f;
+  if (active) beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+  const float ib = ok ? -__fdividef(1.f, beta) : 0.f;       // failed problems: x = 0
+  if constexpr (WTC) {
+    const uint32_t tq = tm + ((uint32_t)(32 * warp) << 16);  // this warp's TMEM lane quarter
+    float av[4][16];                                          // A' row l: A^{-1}[l][v]/beta = ib conj(col[v])
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      av[v >> 3][(2 * v) & 15] = ib * col[v].x;
+      av[v >> 3][(2 * v + 1) & 15] = -ib * col[v].y;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tc::tmem_st16(tq + 16 * c, av[c]);
+    tc::tmem_wait_st();
+    tc::fence_before_sync();
+    named_sync(1, 128);
+    constexpr uint32_t ID = tc::idesc_tf32(128, 32);
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint64_t bb = tc::smem_desc(tc::smem_u32(piece(t)), 512, 128);
+        const uint64_t bs = tc::smem_desc(tc::smem_u32(piece(8 + t)), 512, 128);
+        tc::mma_tf32_ts(tm + 64, tm + 8 * t, bb, ID, t > 0 ? 1u : 0u);   // A'b S'b
+        tc::mma_tf32_ts(tm + 64, tm + 8 * t, bs, ID, 1u);                // A'b S's
+      }
+      tc::mma_commit(&wz_done[0]);
+    }
+    tc::mbar_wait(&wz_done[0], 0);
+    tc::fence_after_sync();
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        av[c][j] = av[c][j] - __uint_as_float(__float_as_uint(av[c][j]) & 0xFFFFE000u);   // A's
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tc::tmem_st16(tq + 16 * c, av[c]);
+    tc::tmem_wait_st();
+    tc::fence_before_sync();
+    named_sync(1, 128);
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        tc::mma_tf32_ts(tm + 64, tm + 8 * t, tc::smem_desc(tc::smem_u32(piece(t)), 512, 128), ID, 1u);   // A's S'b
+      tc::mma_commit(&wz_done[1]);
+    }
+    tc::mbar_wait(&wz_done[1], 0);
+    tc::fence_after_sync();
+    float zv[2][16];
+    tc::tmem_ld16_nowait(tq + 64, zv[0]);
+    tc::tmem_ld16_nowait(tq + 80, zv[1]);
+    tc::tmem_wait_ld();
+    constexpr int KP = (KC + 1) & ~1;
+    float4 *zo = reinterpret_cast<float4 *>(zT + l * FDT_SP);
+#pragma unroll
+    for (int j = 0; j < KP; j += 2) zo[j >> 1] = make_float4(zv[0][j], zv[1][j], zv[0][j + 1], zv[1][j + 1]);
+    tc::fence_before_sync();
+    named_sync(1, 128);                                       // TMEM reads done
+    if (warp == 0) {
+      tc::fence_after_sync();
+      tc::tmem_dealloc(tm, 128);
+    }
+  } else {
+    cp_async_wait_all();
+    __syncwarp();
+    if (active) {                                             // sT[v][k] = s_k[v] (lane v), zero padded
+      constexpr int KP = (KC + 1) & ~1;
+      float4 *row = reinterpret_cast<float4 *>(sT + l * FDT_SP);
+#pragma unroll
+      for (int j = 0; j < KP; j += 2) {
+        const float2 s0 = j < a.K ? ss[j * U + l] : make_float2(0.f, 0.f);
+        const float2 s1 = j + 1 < a.K ? ss[(j + 1) * U + l] : make_float2(0.f, 0.f);
+        row[j >> 1] = make_float4(s0.x, s0.y, s1.x, s1.y);
+      }
+      __syncwarp();
+      whiten_T<KC>(col, ib, sT, zT, a.K, l);
     }
   }
   __syncwarp();
-  whiten_T<KC>(col, ib, sT, zT, a.K, l);
-  __syncwarp();
-  float pw = precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l, FDT_SP);
-  pw = sg_sum<U>(pw);
-  if (l == 0) {
-    a.beta[pr] = ok ? beta : qnan();
-    a.pw[pr] = pw;
-    if (!ok) atomicAdd(a.bad, 1);
+  if (active) {
+    float pw = precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l, FDT_SP);
+    pw = sg_sum<U>(pw);
+    if (l == 0) {
+      a.beta[pr] = ok ? beta : qnan();
+      a.pw[pr] = pw;
+      if (!ok) atomicAdd(a.bad, 1);
+    }
+    fold_b = 1.f / (ok ? beta : qnan());
+    fold_p = pw;
   }
-  fold_b = 1.f / (ok ? beta : qnan());
-  fold_p = pw;
-  }  // active
   pdl_trigger();
   if (a.fold) fd_fold_finish(a, fold, p0, warp, lane, fold_b, fold_p);
 }
