@@ -356,12 +356,14 @@ int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int nprob = a.n_sc * a.groups;
   if constexpr (U == 32) {
     static const bool sg_only = getenv("DP_SOLVE_SG") != nullptr;   // A/B: one warp per problem
-    if (!sg_only) {                                                  // 4 warps per problem (solve_mw.cuh)
-      const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KC) * sizeof(float2);
-      auto kern = dpk::solve_mw_kernel<KC>;
+    static const int nw_env = getenv("DP_SOLVE_NW") ? atoi(getenv("DP_SOLVE_NW")) : 4;
+    if (!sg_only) {                                                  // 4 (or 2) warps per problem (solve_mw.cuh)
+      const int NW = nw_env == 2 ? 2 : 4;
+      const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KC, NW) * sizeof(float2);
+      auto kern = NW == 4 ? dpk::solve_mw_kernel<KC, 4> : dpk::solve_mw_kernel<KC, 2>;
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       LaunchScope ls(c, DP_KERNEL_SOLVE, st);
-      CK(launch_pdl(kern, dim3(nprob), dim3(dpk::SMW_THREADS), sm, st, a));
+      CK(launch_pdl(kern, dim3((nprob + 4 / NW - 1) / (4 / NW)), dim3(dpk::SMW_THREADS), sm, st, a));
       return DP_OK;
     }
   }

@@ -8,12 +8,13 @@
 // Why split: the PD whitening node has one problem per subcarrier (1200 at cfg4), so
 // one warp per problem leaves 2 warps per SM sub-partition and the sweep's serial
 // pivot chain (publish row k+1 -> barrier -> reciprocal -> 32-row update) is exposed.
-// Here lane l of warp w holds column l, rows 8w .. 8w+7: a pivot costs each warp 8
-// row updates (16 FFMA2) instead of 32, four times as many warps are resident, and
-// the pivot chain is a block barrier plus one shared-memory round trip.
+// Here lane l of warp w holds column l, rows (32/NW) w .. : with NW = 2 a pivot costs
+// each warp 16 row updates instead of 32, twice as many warps are resident, and the
+// pivot chain is a 64-thread named barrier plus one shared-memory round trip (NW = 4
+// halves the rows again but doubles the per-pivot overhead instructions).
 //
-// Pivot k lives in warp k/8, register k%8: the 8 pivots of a row block are unrolled
-// (compile-time registers) inside a runtime loop over the 4 blocks, so the code stays
+// Pivot k lives in warp k/R, register k%R: the R pivots of a row block are unrolled
+// (compile-time registers) inside a runtime loop over the NW blocks, so the code stays
 // small.  Look-ahead: during pivot k the owner of row k+1 applies pivot k to that
 // row first, publishes it (and the reciprocal of its diagonal) into the other half of
 // a double-buffered slot; one __syncthreads per pivot separates the buffers' reads
@@ -23,48 +24,27 @@
 
 namespace dpk {
 
-constexpr int SMW_R = 8;      // rows per warp
 constexpr int SMW_THREADS = 128;
 
-__host__ __device__ inline int smw_smem_elems(int K, int KC) {   // complex elements of dynamic smem
-  return npacked(32) + K * 32 + 4 * KC * 32;
+// complex elements of dynamic smem per CTA (4 / NW problems)
+__host__ __device__ inline int smw_smem_elems(int K, int KC, int NW) {
+  return (4 / NW) * (npacked(32) + K * 32 + NW * KC * 32);
 }
 
-template <int KC>
-__global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   // 9 CTAs/SM: 1200 problems in one wave
-  constexpr int U = 32, R = SMW_R;
+// The solve of one problem by NW warps (rows 32/NW per warp, lane l = column l), shared by
+// solve_mw_kernel and the fused PD Gram+solve epilogue (gram_tc2.cuh).  On entry c holds
+// column l, rows R w .. R w + R-1, of A = G + kappa I; `bad` is 0 and visible; `psync`
+// synchronises the NW warps of the problem; ss holds s_k of the problem's subcarrier
+// ([K][U], unless a.Wout) and `part` has NW KC U complex of scratch.  Writes z (or W for
+// a prepare call) and beta of problem p.
+template <int KC, int NW, typename Sync>
+__device__ __forceinline__ void mw_solve(const Args &a, float2 (&c)[32 / NW], int w, int l, int pt, int p,
+                                         bool active, float2 (*slot)[32], float *pinv, float *eqs,
+                                         float (*red)[NW], int &bad, const float2 *ss, float2 *part, Sync psync) {
+  constexpr int U = 32, R = U / NW;
   constexpr int NP = npacked(U);
-  extern __shared__ __align__(16) float2 smw[];
-  float2 *Gs = smw;                 // packed G of the problem
-  float2 *ss = Gs + NP;             // s_k of its subcarrier, [K][U]
-  float2 *part = ss + a.K * U;      // whitening partials [4][KC][U]
-  __shared__ __align__(16) float2 slot[2][U];
-  __shared__ float pinv[2];
-  __shared__ float eqs[U];
-  __shared__ float red[2][4];
-  __shared__ int bad;
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int p = blockIdx.x;
-  const int sc = p / a.groups;
-  if (tid == 0) bad = 0;
-  pdl_wait();
-  for (int i = tid; i < NP / 2; i += SMW_THREADS) cp_async16(Gs + 2 * i, a.G + (size_t)p * NP + 2 * i);
-  if (!a.Wout)                                          // prepare calls have no symbols
-    for (int i = tid; i < a.K * U / 2; i += SMW_THREADS) cp_async16(ss + 2 * i, a.s + (size_t)sc * a.K * U + 2 * i);
-  cp_async_wait_all();
-  __syncthreads();
-
-  // column l of A = G + kappa I, rows R w .. R w + R-1 (Hermitian: lower part mirrored)
-  float2 c[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int u = R * w + r;
-    float2 g = (u <= l) ? Gs[pidx(U, u, l)] : cconj(Gs[pidx(U, l, u)]);
-    if (u == l) g = make_float2(g.x + a.kappa, 0.f);
-    c[r] = g;
-  }
   // Jacobi equilibration A' = D^{-1/2} A D^{-1/2} (unit diagonal)
-  if ((l >> 3) == w) {
+  if (l / R == w) {
     float dl = 0.f;
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -73,7 +53,7 @@ __global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   //
     if (!g) bad = 1;
     eqs[l] = g ? rsqrtf(dl) : 1.f;
   }
-  __syncthreads();
+  psync();
   const float rl = eqs[l];
 #pragma unroll
   for (int r = 0; r < R; ++r) c[r] = cscale(c[r], rl * eqs[R * w + r]);
@@ -87,11 +67,11 @@ __global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   //
       pinv[0] = __fdividef(1.f, g ? d0 : 1.f);
     }
   }
-  __syncthreads();
+  psync();
 
   // ---- sweep: after pivot k, c holds the columns of the partially swept matrix
 #pragma unroll 1
-  for (int kb = 0; kb < U / R; ++kb) {
+  for (int kb = 0; kb < NW; ++kb) {
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int k = R * kb + j;
@@ -121,7 +101,7 @@ __global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   //
         cfms_cj(c[r + 1], hi2(sv), sig);
       }
       if (w == kb) c[j] = piv ? make_float2(-id, 0.f) : cscale(akl, id);   // row k
-      __syncthreads();
+      psync();
     }
   }
   // ---- undo the equilibration: A^{-1} = D^{-1/2} A'^{-1} D^{-1/2};  c = column l of -A^{-1}
@@ -138,23 +118,26 @@ __global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   //
     f += __shfl_xor_sync(0xffffffffu, f, m);
   }
   if (l == 0) { red[0][w] = tr; red[1][w] = f; }
-  __syncthreads();
-  tr = (red[0][0] + red[0][1]) + (red[0][2] + red[0][3]);
-  f = (red[1][0] + red[1][1]) + (red[1][2] + red[1][3]);
+  psync();
+  tr = 0.f;
+  f = 0.f;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) { tr += red[0][i]; f += red[1][i]; }
   // Lemma 1, Eq. (6):  beta^2 = Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)
   const float rad = a.coef * (tr - a.kappa * f);
   const bool ok = (bad == 0) && (rad > 0.f) && (rad < INFINITY);
   const float beta = ok ? sqrtf(rad) : 1.f;
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;   // -: c holds -A^{-1}; failed problems: z = 0
   if (a.Wout) {                                         // prepare: cache W = A^{-1} / beta (upper, packed)
+    if (active) {
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (R * w + r <= l) a.Wout[(size_t)p * NP + pidx(U, R * w + r, l)] = cscale(c[r], ib);
-    if (tid == 0) {
-      a.beta[p] = ok ? beta : qnan();
-      if (!ok) atomicAdd(a.bad, 1);
+      for (int r = 0; r < R; ++r)
+        if (R * w + r <= l) a.Wout[(size_t)p * NP + pidx(U, R * w + r, l)] = cscale(c[r], ib);
+      if (pt == 0) {
+        a.beta[p] = ok ? beta : qnan();
+        if (!ok) atomicAdd(a.bad, 1);
+      }
     }
-    pdl_trigger();
     return;
   }
 
@@ -175,22 +158,73 @@ __global__ void __launch_bounds__(SMW_THREADS, 9) solve_mw_kernel(Args a) {   //
     }
 #pragma unroll
     for (int j = 0; j < KC; ++j) part[(w * KC + j) * U + l] = acc[j];
-    __syncthreads();
-    for (int i = tid; i < KC * U; i += SMW_THREADS) {
+    psync();
+    for (int i = pt; i < KC * U; i += NW * 32) {
       const int j = i / U, u = i % U;
-      if (k0 + j < a.K) {
-        const float2 s0 = part[(0 * KC + j) * U + u], s1 = part[(1 * KC + j) * U + u];
-        const float2 s2 = part[(2 * KC + j) * U + u], s3 = part[(3 * KC + j) * U + u];
-        const float zr = ((s0.x + s1.x) + (s2.x + s3.x)) * ib, zi = ((s0.y + s1.y) + (s2.y + s3.y)) * ib;
-        zo[(size_t)(k0 + j) * U + u] = make_float2(zr, zi);
+      if (active && k0 + j < a.K) {
+        float zr = 0.f, zi = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) {
+          const float2 v = part[(ww * KC + j) * U + u];
+          zr += v.x;
+          zi += v.y;
+        }
+        zo[(size_t)(k0 + j) * U + u] = make_float2(zr * ib, zi * ib);
       }
     }
-    __syncthreads();
+    psync();
   }
-  if (tid == 0) {
+  if (active && pt == 0) {
     a.beta[p] = ok ? beta : qnan();
     if (!ok) atomicAdd(a.bad, 1);
   }
+}
+
+// NW warps per problem (rows 32/NW per warp), 4/NW problems per 128-thread CTA; the
+// warps of one problem synchronise on their own named barrier (id 1 + problem in CTA).
+template <int KC, int NW>
+__global__ void __launch_bounds__(SMW_THREADS, NW == 4 ? 9 : 5) solve_mw_kernel(Args a) {   // 1200 problems in one wave
+  constexpr int U = 32, R = U / NW, PPC = 4 / NW;
+  constexpr int NP = npacked(U);
+  extern __shared__ __align__(16) float2 smw[];
+  __shared__ __align__(16) float2 slot_[PPC][2][U];
+  __shared__ float pinv_[PPC][2];
+  __shared__ float eqs_[PPC][U];
+  __shared__ float red_[PPC][2][NW];
+  __shared__ int bad_[PPC];
+  const int tid = threadIdx.x, l = tid & 31;
+  const int q = (tid >> 5) / NW, w = (tid >> 5) % NW;       // problem in CTA, warp within problem
+  const int pt = tid - q * NW * 32;                         // thread index within the problem
+  const int nprob = a.n_sc * a.groups;
+  const int pr = blockIdx.x * PPC + q;
+  const bool active = pr < nprob;
+  const int p = active ? pr : nprob - 1;
+  const int sc = p / a.groups;
+  float2 *Gs = smw + (size_t)q * (NP + a.K * U + NW * KC * U);
+  float2 *ss = Gs + NP;             // s_k of its subcarrier, [K][U]
+  float2 *part = ss + a.K * U;      // whitening partials [NW][KC][U]
+  int &bad = bad_[q];
+  auto psync = [&]() {
+    if (NW == 4) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NW * 32) : "memory");
+  };
+  if (pt == 0) bad = 0;
+  pdl_wait();
+  for (int i = pt; i < NP / 2; i += NW * 32) cp_async16(Gs + 2 * i, a.G + (size_t)p * NP + 2 * i);
+  if (!a.Wout)                                          // prepare calls have no symbols
+    for (int i = pt; i < a.K * U / 2; i += NW * 32) cp_async16(ss + 2 * i, a.s + (size_t)sc * a.K * U + 2 * i);
+  cp_async_wait_all();
+  psync();
+  // column l of A = G + kappa I, rows R w .. R w + R-1 (Hermitian: lower part mirrored)
+  float2 c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int u = R * w + r;
+    float2 g = (u <= l) ? Gs[pidx(U, u, l)] : cconj(Gs[pidx(U, l, u)]);
+    if (u == l) g = make_float2(g.x + a.kappa, 0.f);
+    c[r] = g;
+  }
+  mw_solve<KC, NW>(a, c, w, l, pt, p, active, slot_[q], pinv_[q], eqs_[q], red_[q], bad, ss, part, psync);
   pdl_trigger();
 }
 
