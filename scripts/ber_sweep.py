@@ -34,25 +34,32 @@ def main():
     ap.add_argument("--n_sc", type=int, default=1200)
     ap.add_argument("--K", type=int, default=14)
     ap.add_argument("--M", type=int, default=64)
+    ap.add_argument("--tau", default="0.125", help="FD regularisation tau_c (Eq. 9); comma list = tau sweep")
+    ap.add_argument("--no-pd", action="store_true", help="FD points only")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     lo, hi, step = (float(v) for v in args.snr.split(":"))
     snrs = [lo + i * step for i in range(int(round((hi - lo) / step)) + 1)]
     Cs = [int(c) for c in args.C.split(",")]
-    run = BerRun(args.n_sc, args.B, args.U, args.K, args.M)
+    taus = [float(t) for t in args.tau.split(",")]
+    runs = {t: BerRun(args.n_sc, args.B, args.U, args.K, args.M, tau=t) for t in taus}
     rows = []
     t0 = time.time()
     for snr in snrs:
-        for mode, C in [("pd", 1)] + [("fd", c) for c in Cs]:
-            e, bits = run.point(mode, C, snr, args.frames)
+        pts = ([] if args.no_pd else [("pd", 1, taus[0])]) + [("fd", c, t) for t in taus for c in Cs]
+        for mode, C, tau in pts:
+            e, bits = runs[tau].point(mode, C, snr, args.frames)
             row = {"mode": "WF(=PD)" if mode == "pd" else "FD", "C": C, "B": args.B, "U": args.U,
                    "snr_db": snr, "errors": e, "bits": bits, "ber": e / bits, "frames": args.frames}
+            if mode == "fd":
+                row["tau"] = tau
             rows.append(row)
             print(json.dumps(row), flush=True)
     torch.cuda.synchronize()
-    run.close()
+    for r in runs.values():
+        r.close()
     meta = {"what": "uncoded BER, Rayleigh, GPU-drawn frames (Philox), libdp precoders", "seconds": time.time() - t0,
-            "n_sc": args.n_sc, "K": args.K, "M": args.M, "tau": 0.125}
+            "n_sc": args.n_sc, "K": args.K, "M": args.M, "tau": taus}
     if args.out:
         with open(args.out, "w") as f:
             json.dump({"meta": meta, "rows": rows}, f, indent=1)
