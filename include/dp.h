@@ -128,6 +128,13 @@ typedef struct {
 #define DP_KERNEL_FINISH        4   /* FD per-subcarrier scalar combination                             */
 #define DP_NUM_KERNELS          5
 
+/* exchange ledger kinds (dp_comm_ledger index): float payload elements this rank hands to */
+#define DP_COMM_GRAM     0  /* PD: allreduce / reduce of the packed Hermitian Gram     */
+#define DP_COMM_S_BCAST  1  /* broadcast of s from rank 0 (FD P:166; PD allreduce topo) */
+#define DP_COMM_Z_BCAST  2  /* PD paper topology: broadcast of z and beta from rank 0           */
+#define DP_COMM_SCALARS  3  /* allreduce of the [n_sc][2] per-subcarrier scalars (rx scale, power)    */
+#define DP_NUM_COMM      4
+
 /* Fill `out128` with a fresh ncclUniqueId (call on rank 0 only, then share the
  * 128 bytes with every rank, e.g. through torch.distributed). */
 DP_API int dp_get_unique_id(void *out128);
@@ -174,6 +181,12 @@ DP_API long long dp_launch_count(dp_ctx *ctx);
 /* Destroy the communicator and free all workspace.  Does not touch caller
  * buffers or streams.  NULL is accepted. */
 DP_API int dp_finalize(dp_ctx *ctx);
+
+/* Exchange ledger: floats[DP_NUM_COMM] = payload elements (fp32) this
+ * rank passed to each kind of collective since the last reset (reset != 0 zeroes them).
+ * Host-side counters: exact and free; compared with the paper's per-link closed forms in
+ * paper_1804_10987_b200/ledger.py. */
+DP_API int dp_comm_ledger(dp_ctx *ctx, long long *floats /*[DP_NUM_COMM]*/, int reset);
 
 /* Thread-local message describing the last error ("" if none). */
 DP_API const char *dp_last_error(void);

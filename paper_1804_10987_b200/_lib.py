@@ -16,6 +16,8 @@ DP_OK, DP_ERR_NUMERIC, DP_ERR_INVALID, DP_ERR_CUDA, DP_ERR_NCCL, DP_ERR_UNSUPPOR
 DP_FLAG_SYNC, DP_FLAG_UNFUSED, DP_FLAG_PROFILE, DP_FLAG_FORCE_COMM = 1, 2, 4, 8
 DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST = 0, 1
 DP_SCALAR_BETA, DP_SCALAR_RX, DP_SCALAR_POWER = 0, 1, 2
+COMM_KINDS = ["gram", "s_bcast", "z_bcast", "scalars"]   # DP_COMM_* order
+DP_NUM_COMM = len(COMM_KINDS)
 KERNEL_NAMES = ["fused_fd", "gram", "solve", "precode", "finish"]
 DP_NUM_KERNELS = len(KERNEL_NAMES)
 
@@ -24,7 +26,7 @@ EXPORTS = [
     "dp_get_unique_id", "dp_init", "dp_precode_pd", "dp_precode_fd", "dp_read_scalars",
     "dp_status", "dp_profile_read", "dp_launch_count", "dp_finalize", "dp_last_error",
     "dp_debug_gram", "dp_debug_solve", "dp_synth_frame", "dp_receive_count",
-    "dp_prepare_pd", "dp_prepare_fd", "dp_apply",
+    "dp_prepare_pd", "dp_prepare_fd", "dp_apply", "dp_comm_ledger",
 ]
 
 
@@ -68,6 +70,7 @@ def lib() -> ctypes.CDLL:
     L.dp_last_error.restype = ctypes.c_char_p
     L.dp_debug_gram.argtypes = [P, P, I, P, P]
     L.dp_debug_solve.argtypes = [P, P, I, P, D, D, P, P, P]
+    L.dp_comm_ledger.argtypes = [P, P, I]
     L.dp_prepare_pd.argtypes = [P, P, D, D, P]
     L.dp_prepare_fd.argtypes = [P, P, D, D, P]
     L.dp_apply.argtypes = [P, P, P, I, P, P]
@@ -165,3 +168,9 @@ def dp_prepare_fd(ctx, H_ptr: int, N0: float, rho2: float, stream: int) -> int:
 
 def dp_apply(ctx, H_ptr: int, s_ptr: int, Ka: int, x_ptr: int, stream: int) -> int:
     return lib().dp_apply(ctx, H_ptr, s_ptr, Ka, x_ptr, stream)
+
+
+def dp_comm_ledger(ctx, reset: bool = False) -> dict:
+    out = (ctypes.c_longlong * DP_NUM_COMM)()
+    check(lib().dp_comm_ledger(ctx, out, int(reset)), "dp_comm_ledger")
+    return {k: int(out[i]) for i, k in enumerate(COMM_KINDS)}

@@ -132,6 +132,10 @@ class Precoder:
         ms, n = L.dp_profile_read(self.ctx, reset)
         return {k: {"ms": ms[i], "launches": n[i]} for i, k in enumerate(L.KERNEL_NAMES)}
 
+    def comm_ledger(self, reset: bool = False) -> dict:
+        """fp32 payload elements this rank handed to each collective kind (include/dp.h DP_COMM_*)."""
+        return L.dp_comm_ledger(self.ctx, reset)
+
     def launch_count(self) -> int:
         return L.dp_launch_count(self.ctx)
 

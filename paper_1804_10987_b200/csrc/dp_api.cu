@@ -61,6 +61,9 @@ int fail(int code, const char *fmt, ...) {
     if (rc_ != DP_OK) return rc_; \
   } while (0)
 
+// count a collective's payload (floats) in the context's exchange ledger
+#define LEDGER(c, kind, nfloats) ((c)->ledger[(kind)] += (long long)(nfloats))
+
 struct ProfRec {
   int kid;
   cudaEvent_t a, b;
@@ -102,6 +105,8 @@ struct dp_ctx {
   double prof_ms[DP_NUM_KERNELS] = {0};
   long long prof_n[DP_NUM_KERNELS] = {0};
   long long launches = 0;
+  // exchange ledger: float payload elements handed to each kind of collective by this rank
+  long long ledger[DP_NUM_COMM] = {0};
 };
 
 namespace {
@@ -648,9 +653,11 @@ int distribute_s(dp_ctx *c, const float2 *s, cudaStream_t st, const float2 **s_u
   const size_t n = (size_t)c->cfg.n_sc * (K > 0 ? K : c->cfg.K) * c->cfg.U * 2;
   if (c->cfg.rank == 0) {
     NK(ncclBroadcast(s, (void *)s, n, ncclFloat, 0, c->comm, st));
+    LEDGER(c, DP_COMM_S_BCAST, n);
     *s_use = s;
   } else {
     NK(ncclBroadcast(nullptr, c->s_buf, n, ncclFloat, 0, c->comm, st));
+    LEDGER(c, DP_COMM_S_BCAST, n);
     *s_use = c->s_buf;
   }
   return DP_OK;
@@ -826,7 +833,10 @@ int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
       CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
     }
   }
-  if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+  if (c->comm_on) {
+    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
+  }
   c->last_mode = 1;
   c->prepared = -1;                                       // G workspace reused
   return finish_call(c, host, x, st);
@@ -866,9 +876,11 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
   if (c->comm_on && !topo_t1) {
     // cross-rank adder tree on every rank; every rank whitens redundantly
     NK(ncclAllReduce(c->G, c->G, nG, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_GRAM, nG);
   } else if (topo_t1) {
     // paper topology: reduce the Grams to the master GPU
     NK(ncclReduce(c->G, c->G, nG, ncclFloat, ncclSum, 0, c->comm, st));
+    LEDGER(c, DP_COMM_GRAM, nG);
   }
   // (b) whitening node: A = G + kappa I, LDL^H, A^{-1}, beta (Lemma 1), z = A^{-1} s / beta
   if (!topo_t1 || k.rank == 0) RET(dispatch<Solve>(k.U, k.K, c, a, st));
@@ -878,6 +890,7 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
     NK(ncclBroadcast(c->z, c->z, (size_t)k.n_sc * k.K * k.U * 2, ncclFloat, 0, c->comm, st));
     NK(ncclBroadcast(c->beta, c->beta, (size_t)k.n_sc, ncclFloat, 0, c->comm, st));
     NK(ncclGroupEnd());
+    LEDGER(c, DP_COMM_Z_BCAST, (size_t)k.n_sc * k.K * k.U * 2 + (size_t)k.n_sc);
   }
   // (c) local precode x_c = H_c^H z on every rank
   a.zin = c->z;
@@ -892,7 +905,10 @@ int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double
     RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
   }
   // per-subcarrier scalars (written by the precode kernel): power summed over ranks
-  if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+  if (c->comm_on) {
+    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
+  }
   c->last_mode = 0;
   c->prepared = -1;
   return finish_call(c, host, x, st);
@@ -963,6 +979,16 @@ int dp_profile_read(dp_ctx *c, double *ms, long long *launches, int reset) {
 }
 
 long long dp_launch_count(dp_ctx *c) { return c ? c->launches : 0; }
+
+int dp_comm_ledger(dp_ctx *c, long long *floats, int reset) {
+  g_err.clear();
+  if (!c || !floats) return fail(DP_ERR_INVALID, "NULL argument");
+  for (int i = 0; i < DP_NUM_COMM; ++i) {
+    floats[i] = c->ledger[i];
+    if (reset) c->ledger[i] = 0;
+  }
+  return DP_OK;
+}
 
 int dp_finalize(dp_ctx *c) {
   if (!c) return DP_OK;
@@ -1038,6 +1064,7 @@ int dp_prepare_pd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
   RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));   // G_c summed over local clusters
   if (c->comm_on)                                         // every rank holds sum_c G_c
     NK(ncclAllReduce(c->G, c->G, (size_t)k.n_sc * dpk::npacked(k.U) * 2, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_GRAM, (size_t)k.n_sc * dpk::npacked(k.U) * 2);
   a.G = c->G;
   a.Wout = c->G;                                          // W = A^{-1}/beta in place of G
   a.s = nullptr;
@@ -1117,7 +1144,10 @@ int dp_apply(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, int Ka, dp_c32 *x, voi
     if (precode_tc2_ok(c, a)) RET(launch_precode_tc2(c, a, st));
     else RET(dispatch<Precode>(k.U, Ka, c, a, c->pd_nw, st));
   }
-  if (c->comm_on) NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+  if (c->comm_on) {
+    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
+  }
   c->last_mode = c->prepared;
   if (k.flags & DP_FLAG_SYNC) {
     CK(cudaStreamSynchronize(st));
