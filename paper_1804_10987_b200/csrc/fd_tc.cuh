@@ -153,9 +153,6 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ uint32_t map_rank(const void *p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tc::smem_u32(p)), "r"(rank));
@@ -166,6 +163,9 @@ __device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t r
                "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
                : "memory");
 }
+// The cluster barrier that orders rank 0's mbarrier init before the other ranks' st.async is
+// split: arrive (release) at kernel start, wait (acquire) only just before the push at the
+// end, by which time every CTA of the cluster has long arrived — no stall at kernel start.
 __device__ __forceinline__ void fd_fold_init(const Args &a, FoldSmem &f) {
   if (a.fold > 1) {
     if (threadIdx.x == 0 && cluster_rank() == 0) {
@@ -173,7 +173,7 @@ __device__ __forceinline__ void fd_fold_init(const Args &a, FoldSmem &f) {
       tc::fence_mbar_init();
       tc::mbar_arrive_expect_tx(&f.bar, 32u * (a.fold - 1));
     }
-    cluster_sync_all();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   }
 }
 __device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p0, int warp, int lane, float ib, float pw) {
@@ -193,6 +193,7 @@ __device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p
     }
     return;
   }
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // pairs with fd_fold_init
   if (threadIdx.x != 0) return;
   const uint32_t rank = cluster_rank();
   if (rank != 0) {                                             // push to rank 0 and leave
