@@ -96,6 +96,7 @@ struct dp_ctx {
   size_t pw_len = 0;
   // host staging (host-pointer calls)
   float2 *h_dev = nullptr, *s_dev = nullptr, *x_dev = nullptr;
+  cudaStream_t st_h2d = nullptr, st_d2h = nullptr;   // host-pointer pipeline copy streams
   // last call
   int last_mode = -1;        // 0 pd, 1 fd
   int prepared = -1;         // W cached in G by dp_prepare_pd (0) / dp_prepare_fd (1); -1 none
@@ -677,6 +678,199 @@ int finish_call(dp_ctx *c, bool host, dp_c32 *x, cudaStream_t st) {
   return DP_OK;
 }
 
+// FD frame on device pointers (everything after the host staging)
+int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, double rho2, float2 *xd,
+                   cudaStream_t st) {
+  const dp_config &k = c->cfg;
+  const float2 *s_use;
+  RET(distribute_s(c, sd, st, &s_use));
+  // FD parameters (Sec. III-C): rho_c^2 = rho^2/C (P:215), kappa_c = tau U N0 / rho_c^2 (Eq. 9)
+  const double rho_c2 = rho2 / k.C;
+  Args a = base_args(c);
+  a.H = Hd;
+  a.s = s_use;
+  a.x = xd;
+  a.S = c->S;
+  a.nchunks = c->Cl;
+  a.kappa = (float)(k.tau * k.U * N0 / rho_c2);
+  a.coef = (float)(k.Es / rho_c2);
+  a.nbeta = c->Cl;
+  if (c->S < k.U) {
+    // small clusters (B_c < U, P:227-233): B_c x B_c regularised Gram per cluster
+    RET(launch_fd_small(c, a, st));
+    LaunchScope ls(c, DP_KERNEL_FINISH, st);
+    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+  } else if (k.flags & DP_FLAG_UNFUSED) {
+    // (a) per-cluster Grams -> (b) solve+whiten per cluster -> (c) precode
+    a.Gout = c->G;
+    RET(dispatch<GramPer>(k.U, k.K, c, a, c->fdu_nw, st));
+    a.G = c->G;
+    a.groups = c->Cl;
+    a.zout = c->z;
+    RET(dispatch<Solve>(k.U, k.K, c, a, st));
+    a.zin = c->z;
+    a.zgroups = c->Cl;
+    a.chunks_per_zgroup = 1;
+    RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
+  } else {
+    const bool tc = fd_tc_ok(c, a);
+    if (tc) RET(launch_fd_tc_kc(c, a, st));
+    else RET(dispatch<FdFused>(k.U, k.K, c, a, st));
+    if (!tc || fd_fold_of(c, a) == 0) {                       // scalars not folded into the kernel
+      LaunchScope ls(c, DP_KERNEL_FINISH, st);
+      CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+    }
+  }
+  if (c->comm_on) {
+    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
+  }
+  c->last_mode = 1;
+  c->prepared = -1;                                       // G workspace reused
+  return DP_OK;
+}
+
+// PD frame on device pointers (everything after the host staging)
+int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, double rho2, float2 *xd,
+                   cudaStream_t st) {
+  const dp_config &k = c->cfg;
+  // PD parameters (Theorem 1, Eq. 5): kappa = U N0 / rho^2 ; beta via Lemma 1 with rho^2
+  Args a = base_args(c);
+  a.H = Hd;
+  a.x = xd;
+  a.S = c->pd_chunk;
+  a.nchunks = c->pd_nchunks;
+  a.kappa = (float)(k.U * N0 / rho2);
+  a.coef = (float)(k.Es / rho2);
+  a.groups = 1;
+  a.nbeta = 1;
+  a.fin_inv_beta = (k.rank == 0) ? 1 : 0;   // 1/beta contributed once to the scalar allreduce
+  const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
+  const float2 *s_use = sd;
+  if (!topo_t1) RET(distribute_s(c, sd, st, &s_use));   // T2: overlaps nothing yet; only s crosses
+  a.s = s_use;
+  // (a) Gram of this rank's antennas: first levels of the adder tree G = sum_c G_c (P:181)
+  const size_t nG = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
+  a.Gout = c->G;
+  RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
+  a.G = c->G;
+  a.zout = c->z;
+  if (c->comm_on && !topo_t1) {
+    // cross-rank adder tree on every rank; every rank whitens redundantly
+    NK(ncclAllReduce(c->G, c->G, nG, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_GRAM, nG);
+  } else if (topo_t1) {
+    // paper topology (P:280-281): reduce the Grams to the master GPU
+    NK(ncclReduce(c->G, c->G, nG, ncclFloat, ncclSum, 0, c->comm, st));
+    LEDGER(c, DP_COMM_GRAM, nG);
+  }
+  // (b) whitening node: A = G + kappa I, LDL^H, A^{-1}, beta (Lemma 1), z = A^{-1} s / beta
+  if (!topo_t1 || k.rank == 0) RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  if (topo_t1) {
+    // master broadcasts z (P:296) and beta
+    NK(ncclGroupStart());
+    NK(ncclBroadcast(c->z, c->z, (size_t)k.n_sc * k.K * k.U * 2, ncclFloat, 0, c->comm, st));
+    NK(ncclBroadcast(c->beta, c->beta, (size_t)k.n_sc, ncclFloat, 0, c->comm, st));
+    NK(ncclGroupEnd());
+    LEDGER(c, DP_COMM_Z_BCAST, (size_t)k.n_sc * k.K * k.U * 2 + (size_t)k.n_sc);
+  }
+  // (c) local precode x_c = H_c^H z on every rank (P:178, P:296)
+  a.zin = c->z;
+  a.zgroups = 1;
+  a.chunks_per_zgroup = c->pd_nchunks;
+  if (precode_tc2_ok(c, a)) {
+    RET(launch_precode_tc2(c, a, st));               // tensor-core precode, writes the scalars
+  } else if (precode_tc_ok(c, a)) {
+    RET(launch_precode_tc(c, a, st));                // tensor-core precode (+ scalar finish)
+    RET(launch_finish(c, a, st));
+  } else {
+    RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
+  }
+  // per-subcarrier scalars (written by the precode kernel): power summed over ranks
+  if (c->comm_on) {
+    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
+  }
+  c->last_mode = 0;
+  c->prepared = -1;
+  return DP_OK;
+}
+
+// Host-pointer frames, world = 1: the frame is cut into subcarrier chunks (subcarriers are
+// independent problems) and H2D of chunk i+1, the kernels of chunk i and D2H of chunk i-1
+// overlap on three streams (copy engines both ways + compute), instead of copy-all /
+// compute / copy-all.  The scalar outputs (beta, fin) are written at the chunk's offset;
+// the other workspace is reused chunk after chunk on the compute stream.
+using DevFn = int (*)(dp_ctx *, const float2 *, const float2 *, double, double, float2 *, cudaStream_t);
+int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c32 *s, double N0, double rho2,
+                   dp_c32 *x, cudaStream_t st) {
+  const dp_config k = c->cfg;
+  const int nch = std::min(8, k.n_sc);
+  const size_t rowH = (size_t)c->Bl * k.U, rowS = (size_t)k.K * k.U, rowX = (size_t)k.K * c->Bl;
+  if (!c->h_dev) {
+    RET(alloc((void **)&c->h_dev, (size_t)k.n_sc * rowH * 8));
+    RET(alloc((void **)&c->s_dev, (size_t)k.n_sc * rowS * 8));
+    RET(alloc((void **)&c->x_dev, (size_t)k.n_sc * rowX * 8));
+  }
+  if (!c->st_h2d) {
+    CK(cudaStreamCreateWithFlags(&c->st_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->st_d2h, cudaStreamNonBlocking));
+  }
+  cudaEvent_t ev_start = take_event(c);
+  CK(cudaEventRecord(ev_start, st));                       // after the caller's prior work
+  CK(cudaStreamWaitEvent(c->st_h2d, ev_start, 0));
+  float *beta0 = c->beta, *fin0 = c->fin;
+  int rc = DP_OK;
+  std::vector<cudaEvent_t> evs;
+  for (int i = 0; i < nch && rc == DP_OK; ++i) {
+    const int sc0 = (int)((long long)k.n_sc * i / nch), sc1 = (int)((long long)k.n_sc * (i + 1) / nch);
+    const int n = sc1 - sc0;
+    cudaEvent_t ein = take_event(c), eout = take_event(c);
+    evs.push_back(ein);
+    evs.push_back(eout);
+    CK(cudaMemcpyAsync(c->h_dev + sc0 * rowH, H + sc0 * rowH, n * rowH * 8, cudaMemcpyHostToDevice, c->st_h2d));
+    CK(cudaMemcpyAsync(c->s_dev + sc0 * rowS, s + sc0 * rowS, n * rowS * 8, cudaMemcpyHostToDevice, c->st_h2d));
+    CK(cudaEventRecord(ein, c->st_h2d));
+    CK(cudaStreamWaitEvent(st, ein, 0));
+    c->cfg.n_sc = n;                                        // chunk view of the context
+    c->beta = beta0 + (size_t)sc0 * groups;
+    c->fin = fin0 + (size_t)sc0 * 2;
+    rc = fn(c, c->h_dev + sc0 * rowH, c->s_dev + sc0 * rowS, N0, rho2, c->x_dev + sc0 * rowX, st);
+    c->cfg.n_sc = k.n_sc;
+    c->beta = beta0;
+    c->fin = fin0;
+    if (rc != DP_OK) break;
+    CK(cudaEventRecord(eout, st));
+    CK(cudaStreamWaitEvent(c->st_d2h, eout, 0));
+    CK(cudaMemcpyAsync(x + sc0 * rowX, c->x_dev + sc0 * rowX, n * rowX * 8, cudaMemcpyDeviceToHost, c->st_d2h));
+  }
+  CK(cudaStreamSynchronize(c->st_d2h));
+  CK(cudaStreamSynchronize(st));
+  for (auto e : evs) c->ev_pool.push_back(e);
+  c->ev_pool.push_back(ev_start);
+  return rc;
+}
+
+int precode_entry(dp_ctx *c, bool fd, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x,
+                  void *stream) {
+  g_err.clear();
+  RET(validate_call(c, H, s, N0, rho2, x));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->cfg.device));
+  DevFn fn = fd ? precode_fd_dev : precode_pd_dev;
+  const bool hdev = is_device_ptr(H);
+  static const bool no_pipe = getenv("DP_NO_HOST_PIPELINE") != nullptr;
+  if (!hdev && !c->comm_on && !no_pipe && s && !is_device_ptr(x) && !is_device_ptr(s) && c->cfg.n_sc >= 16) {
+    RET(host_pipelined(c, fn, fd ? c->Cl : 1, H, s, N0, rho2, x, st));
+    return finish_call(c, false, x, st);                    // numeric check (DP_FLAG_SYNC); data already home
+  }
+  bool host;
+  const float2 *Hd, *sd;
+  float2 *xd;
+  RET(stage_in(c, H, s, x, st, &host, &Hd, &sd, &xd));
+  RET(fn(c, Hd, sd, N0, rho2, xd, st));
+  return finish_call(c, host, x, st);
+}
 }  // namespace
 
 // ====================================================================== C ABI
@@ -785,134 +979,12 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
 }
 
 int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
-  g_err.clear();
-  RET(validate_call(c, H, s, N0, rho2, x));
-  cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaSetDevice(c->cfg.device));
-  const dp_config &k = c->cfg;
-  bool host;
-  const float2 *Hd, *sd;
-  float2 *xd;
-  RET(stage_in(c, H, s, x, st, &host, &Hd, &sd, &xd));
-  const float2 *s_use;
-  RET(distribute_s(c, sd, st, &s_use));
-  // FD parameters (Sec. III-C): rho_c^2 = rho^2/C (P:215), kappa_c = tau U N0 / rho_c^2 (Eq. 9)
-  const double rho_c2 = rho2 / k.C;
-  Args a = base_args(c);
-  a.H = Hd;
-  a.s = s_use;
-  a.x = xd;
-  a.S = c->S;
-  a.nchunks = c->Cl;
-  a.kappa = (float)(k.tau * k.U * N0 / rho_c2);
-  a.coef = (float)(k.Es / rho_c2);
-  a.nbeta = c->Cl;
-  if (c->S < k.U) {
-    // small clusters (B_c < U, P:227-233): B_c x B_c regularised Gram per cluster
-    RET(launch_fd_small(c, a, st));
-    LaunchScope ls(c, DP_KERNEL_FINISH, st);
-    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
-  } else if (k.flags & DP_FLAG_UNFUSED) {
-    // (a) per-cluster Grams -> (b) solve+whiten per cluster -> (c) precode
-    a.Gout = c->G;
-    RET(dispatch<GramPer>(k.U, k.K, c, a, c->fdu_nw, st));
-    a.G = c->G;
-    a.groups = c->Cl;
-    a.zout = c->z;
-    RET(dispatch<Solve>(k.U, k.K, c, a, st));
-    a.zin = c->z;
-    a.zgroups = c->Cl;
-    a.chunks_per_zgroup = 1;
-    RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
-  } else {
-    const bool tc = fd_tc_ok(c, a);
-    if (tc) RET(launch_fd_tc_kc(c, a, st));
-    else RET(dispatch<FdFused>(k.U, k.K, c, a, st));
-    if (!tc || fd_fold_of(c, a) == 0) {                       // scalars not folded into the kernel
-      LaunchScope ls(c, DP_KERNEL_FINISH, st);
-      CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
-    }
-  }
-  if (c->comm_on) {
-    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
-    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
-  }
-  c->last_mode = 1;
-  c->prepared = -1;                                       // G workspace reused
-  return finish_call(c, host, x, st);
+  return precode_entry(c, true, H, s, N0, rho2, x, stream);
+}
+int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
+  return precode_entry(c, false, H, s, N0, rho2, x, stream);
 }
 
-int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
-  g_err.clear();
-  RET(validate_call(c, H, s, N0, rho2, x));
-  cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaSetDevice(c->cfg.device));
-  const dp_config &k = c->cfg;
-  bool host;
-  const float2 *Hd, *sd;
-  float2 *xd;
-  RET(stage_in(c, H, s, x, st, &host, &Hd, &sd, &xd));
-  // PD parameters (Theorem 1, Eq. 5): kappa = U N0 / rho^2 ; beta via Lemma 1 with rho^2
-  Args a = base_args(c);
-  a.H = Hd;
-  a.x = xd;
-  a.S = c->pd_chunk;
-  a.nchunks = c->pd_nchunks;
-  a.kappa = (float)(k.U * N0 / rho2);
-  a.coef = (float)(k.Es / rho2);
-  a.groups = 1;
-  a.nbeta = 1;
-  a.fin_inv_beta = (k.rank == 0) ? 1 : 0;   // 1/beta contributed once to the scalar allreduce
-  const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
-  const float2 *s_use = sd;
-  if (!topo_t1) RET(distribute_s(c, sd, st, &s_use));   // T2: overlaps nothing yet; only s crosses
-  a.s = s_use;
-  // (a) Gram of this rank's antennas: first levels of the adder tree G = sum_c G_c (P:181)
-  const size_t nG = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
-  a.Gout = c->G;
-  RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
-  a.G = c->G;
-  a.zout = c->z;
-  if (c->comm_on && !topo_t1) {
-    // cross-rank adder tree on every rank; every rank whitens redundantly
-    NK(ncclAllReduce(c->G, c->G, nG, ncclFloat, ncclSum, c->comm, st));
-    LEDGER(c, DP_COMM_GRAM, nG);
-  } else if (topo_t1) {
-    // paper topology (P:280-281): reduce the Grams to the master GPU
-    NK(ncclReduce(c->G, c->G, nG, ncclFloat, ncclSum, 0, c->comm, st));
-    LEDGER(c, DP_COMM_GRAM, nG);
-  }
-  // (b) whitening node: A = G + kappa I, LDL^H, A^{-1}, beta (Lemma 1), z = A^{-1} s / beta
-  if (!topo_t1 || k.rank == 0) RET(dispatch<Solve>(k.U, k.K, c, a, st));
-  if (topo_t1) {
-    // master broadcasts z (P:296) and beta
-    NK(ncclGroupStart());
-    NK(ncclBroadcast(c->z, c->z, (size_t)k.n_sc * k.K * k.U * 2, ncclFloat, 0, c->comm, st));
-    NK(ncclBroadcast(c->beta, c->beta, (size_t)k.n_sc, ncclFloat, 0, c->comm, st));
-    NK(ncclGroupEnd());
-    LEDGER(c, DP_COMM_Z_BCAST, (size_t)k.n_sc * k.K * k.U * 2 + (size_t)k.n_sc);
-  }
-  // (c) local precode x_c = H_c^H z on every rank (P:178, P:296)
-  a.zin = c->z;
-  a.zgroups = 1;
-  a.chunks_per_zgroup = c->pd_nchunks;
-  if (precode_tc2_ok(c, a)) {
-    RET(launch_precode_tc2(c, a, st));               // tensor-core precode, writes the scalars
-  } else if (precode_tc_ok(c, a)) {
-    RET(launch_precode_tc(c, a, st));                // tensor-core precode (+ scalar finish)
-    RET(launch_finish(c, a, st));
-  } else {
-    RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
-  }
-  // per-subcarrier scalars (written by the precode kernel): power summed over ranks
-  if (c->comm_on) {
-    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
-    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
-  }
-  c->last_mode = 0;
-  c->prepared = -1;
-  return finish_call(c, host, x, st);
-}
 
 int dp_read_scalars(dp_ctx *c, int which, float *dst, void *stream) {
   g_err.clear();
@@ -997,6 +1069,8 @@ int dp_finalize(dp_ctx *c) {
   drain_profile(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->st_h2d) cudaStreamDestroy(c->st_h2d);
+  if (c->st_d2h) cudaStreamDestroy(c->st_d2h);
   void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev};
   for (void *b : bufs)
     if (b) cudaFree(b);

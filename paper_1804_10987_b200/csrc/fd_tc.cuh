@@ -173,7 +173,7 @@ __device__ __forceinline__ void fd_fold_init(const Args &a, FoldSmem &f) {
       tc::fence_mbar_init();
       tc::mbar_arrive_expect_tx(&f.bar, 32u * (a.fold - 1));
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // init already fenced (fence.mbarrier_init)
   }
 }
 __device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p0, int warp, int lane, float ib, float pw) {

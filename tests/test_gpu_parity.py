@@ -224,6 +224,26 @@ def test_host_pointer_path_matches_device_path(pinned):
     assert np.array_equal(xh_pd.numpy(), xd_pd) and np.array_equal(xh_fd.numpy(), xd_fd)
 
 
+@pytest.mark.parametrize("cfgid", [3, 4])
+def test_host_pipeline_chunks_scalars(cfgid):
+    """Host-pointer frames run chunked (H2D / kernels / D2H overlapped over subcarrier chunks):
+    x and the per-subcarrier scalars of every chunk equal the device-pointer frame's."""
+    cfg = CONFIGS[cfgid]
+    f = frame(cfg, 45)
+    for mode in ("pd", "fd"):
+        xd, bd, rxd, pwd, _ = run(cfg, f, mode, 0.1)
+        with Precoder(45, cfg.B, cfg.U, cfg.K, cfg.C, tau=cfg.tau) as pre:
+            H = torch.from_numpy(f.H).pin_memory()
+            s = torch.from_numpy(f.s).pin_memory()
+            xh = (pre.precode_pd if mode == "pd" else pre.precode_fd)(H, s, 0.1, 1.0)
+            bh = pre.read_scalars("beta").cpu().numpy()
+            rxh = pre.read_scalars("rx").cpu().numpy()
+            pwh = pre.read_scalars("power").cpu().numpy()
+            assert pre.status() == 0
+        assert np.array_equal(xh.numpy(), xd), mode
+        assert np.array_equal(bh, bd) and np.array_equal(rxh, rxd) and np.array_equal(pwh, pwd), mode
+
+
 @pytest.mark.parametrize("C", [1, 2, 4, 8])
 def test_fd_u32_cluster_counts(C):
     """U = 32, S = 32 (tensor-core FD kernel) for every way the per-subcarrier scalars
