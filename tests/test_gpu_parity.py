@@ -114,10 +114,13 @@ def test_parity_full_size_sampled(cfgid, mode):
     assert abs(np.mean(pw) / cfg.K - 1.0) < 0.05 if mode == "pd" else True
 
 
-@pytest.mark.parametrize("K", [1, 7, 14, 16])
-def test_symbol_counts(K):
-    base = CONFIGS[3]
-    cfg = synth_cfg = type(base)(base.cfg_id, "k", 21, base.B, base.U, base.C, K, base.M)
+@pytest.mark.parametrize("cfgid", [3, 4])
+@pytest.mark.parametrize("K", [1, 7, 14, 16, 17, 40])
+def test_symbol_counts(cfgid, K):
+    """K = 1 .. 40 symbols per frame: K <= 16 takes the tensor-core paths at U = 32, K > 16 the
+    SIMT kernels in chunks of 16 symbols."""
+    base = CONFIGS[cfgid]
+    cfg = type(base)(base.cfg_id, "k", 21, base.B, base.U, base.C, K, base.M)
     f = frame(cfg)
     N0 = 0.1
     for mode in ("pd", "fd"):
@@ -244,6 +247,24 @@ def test_host_pipeline_chunks_scalars(cfgid):
         assert np.array_equal(bh, bd) and np.array_equal(rxh, rxd) and np.array_equal(pwh, pwd), mode
 
 
+@pytest.mark.parametrize("Bl", [32, 64, 128])
+@pytest.mark.parametrize("mode", ["pd", "fd"])
+def test_u32_per_rank_shapes(Bl, mode):
+    """The per-rank shapes of cfg4 (B = 256, U = 32, C = 8) on 8, 4 and 2 GPUs run at world = 1:
+    B_local = 32 / 64 / 128 with 1 / 2 / 4 clusters (Gram with 32- / 64-antenna chunks, SIMT
+    or tensor-core precode, in-CTA scalar folding, SIMT whitening when a CTA spans subcarriers)."""
+    base = CONFIGS[4]
+    cfg = type(base)(base.cfg_id, f"rank{Bl}", 27, Bl, 32, Bl // 32, 14, 64)
+    f = frame(cfg)
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    x, beta, rx, pw, nbad = run(cfg, f, mode, N0)
+    xr, br, rxr = reference(cfg, f, mode, N0)
+    assert nbad == 0
+    assert rel_l2(x, xr) <= REL_TOL, rel_l2(x, xr)
+    assert np.max(np.abs(rx / rxr - 1)) <= REL_TOL
+    assert np.max(np.abs(pw / np.sum(np.abs(xr) ** 2, axis=(1, 2)) - 1)) <= 1e-4
+
+
 @pytest.mark.parametrize("C", [1, 2, 4, 8])
 def test_fd_u32_cluster_counts(C):
     """U = 32, S = 32 (tensor-core FD kernel) for every way the per-subcarrier scalars
@@ -351,10 +372,11 @@ def test_fd_single_cluster_tau1_equals_pd():
     assert rel_l2(x_fd, x_pd) <= 1e-5
 
 
-def test_force_comm_world1_paths():
+@pytest.mark.parametrize("cfgid", [3, 4])
+def test_force_comm_world1_paths(cfgid):
     """NCCL code path with a 1-rank communicator: PD allreduce topology, PD paper
     topology (reduce + z broadcast) and FD (s broadcast + scalar allreduce)."""
-    cfg = CONFIGS[3]
+    cfg = CONFIGS[cfgid]
     f = frame(cfg, 31)
     N0 = 0.1
     uid = L.dp_get_unique_id()
