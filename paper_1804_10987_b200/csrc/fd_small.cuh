@@ -27,6 +27,8 @@ __host__ __device__ inline int fds_size(int K) {
 
 template <int S, int U, int KC>
 __global__ void __launch_bounds__(128) fd_small_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
   constexpr int PPW = 32 / S;
   extern __shared__ __align__(16) float2 smem[];

@@ -214,6 +214,8 @@ __device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p
 // WTC: whitening on the tensor cores (see below); false: SIMT whitening (whiten_T)
 template <int KC, bool WTC>
 __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   constexpr int U = 32;
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   // align by an offset (not integer casts) so the compiler keeps the shared state space: LDS, not LD

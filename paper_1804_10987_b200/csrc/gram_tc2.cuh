@@ -39,6 +39,8 @@ template <int CH> struct GT2 {
 
 template <int CH>
 __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   using T = GT2<CH>;
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);

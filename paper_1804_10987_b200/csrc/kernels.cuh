@@ -721,6 +721,8 @@ __device__ __forceinline__ void finish_sc(const Args &a, int sc) {
 // smem per SG: tile S*U + scratch U + max(U/2 (U/2 + 2), K*U + U*zs).
 template <int U, int KC>
 __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
@@ -786,6 +788,8 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
 // smem: [tile Bl*U][tree (nw/2) * 32 * (3U/4) complex]
 template <int U, bool PER_CHUNK>
 __global__ void __launch_bounds__(256) gram_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
   constexpr int PPW = 32 / U;
   constexpr int NE = U / 2 + U / 4;
@@ -845,6 +849,8 @@ __global__ void __launch_bounds__(256) gram_kernel(Args a) {
 // -> beta -> z = A^{-1} s / beta (written as z[p][k][u]).  4 warps per CTA.
 template <int U, int KC>
 __global__ void __launch_bounds__(128) solve_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
@@ -900,6 +906,8 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
 // the whitening matrix is computed once per channel and applied to every symbol).
 template <int U, int KC>
 __global__ void __launch_bounds__(128) whiten_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
   constexpr int PPW = 32 / U;
   constexpr int NP = npacked(U);
@@ -934,6 +942,8 @@ __global__ void __launch_bounds__(128) whiten_kernel(Args a) {
 // smem: [tile Bl*U][zT zgroups*U*zs]
 template <int U, int KC>
 __global__ void __launch_bounds__(256) precode_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
@@ -974,6 +984,8 @@ __global__ void __launch_bounds__(256) precode_kernel(Args a) {
 // sum_c power_c}.  (A separate grid: folding it into the fused kernel needs a
 // release fence per cluster, which waits for that warp's x stores and cost ~10%.)
 __global__ void __launch_bounds__(128) fd_finish_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
   const int sc = blockIdx.x * blockDim.x + threadIdx.x;
   if (sc < a.n_sc) finish_sc(a, sc);

@@ -42,6 +42,8 @@ constexpr int PC2_THREADS = 320;
 constexpr size_t PC2_SMEM = (size_t)(PC2_NS + PC2_NH) * PC2_STAGE + 2 * PC2_ZOP + 1024;
 
 __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
   uint8_t *hsb = sm + (size_t)PC2_NS * PC2_STAGE;   // residual buffers

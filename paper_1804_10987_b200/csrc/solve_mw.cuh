@@ -183,7 +183,9 @@ __device__ __forceinline__ void mw_solve(const Args &a, float2 (&c)[32 / NW], in
 // NW warps per problem (rows 32/NW per warp), 4/NW problems per 128-thread CTA; the
 // warps of one problem synchronise on their own named barrier (id 1 + problem in CTA).
 template <int KC, int NW>
-__global__ void __launch_bounds__(SMW_THREADS, NW == 4 ? 9 : 5) solve_mw_kernel(Args a) {   // 1200 problems in one wave
+__global__ void __launch_bounds__(SMW_THREADS, NW == 4 ? 9 : 5) solve_mw_kernel(Args a) {
+  pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
+                   // (it still waits for this grid's completion in griddepcontrol.wait)   // 1200 problems in one wave
   constexpr int U = 32, R = U / NW, PPC = 4 / NW;
   constexpr int NP = npacked(U);
   extern __shared__ __align__(16) float2 smw[];
