@@ -440,6 +440,8 @@ def main():
             per[k] = {"bound": "alu", "flops": f_, "achieved_tflops": f_ / (kms / 1e3) / 1e12,
                       "frac": f_ / (kms / 1e3) / 1e12 / fp32_peak,
                       "tensor_core_gram_flops": cfg.n_sc * Cl * flf["gram"] if cfg.U == 32 else 0.0}
+        else:                                    # fd_finish_kernel (U < 32): per-subcarrier scalars
+            per[k] = {"bound": "latency", "note": "tiny per-subcarrier combine"}
         per[k]["ms_avg"] = kms
     roof["per_kernel"] = per
 

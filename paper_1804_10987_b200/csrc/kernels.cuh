@@ -587,7 +587,12 @@ __device__ __forceinline__ float sweep_sg2(float2 (&w)[U], float2 *slot, int l, 
   f = sg_sum<U>(f);
   // Lemma 1, Eq. (6):  beta^2 = Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)
   const float r = coef * (tr - kappa * f);
-  ok = __all_sync(0xffffffffu, gd) && (pmin > 0.f) && (pmax < INFINITY) && (r > 0.f) && (r < INFINITY);
+  const bool all_gd = sg_sum<U>(gd ? 0.f : 1.f) == 0.f;   // every diagonal of this problem valid
+  ok = all_gd && (pmin > 0.f) && (pmax < INFINITY) && (r > 0.f) && (r < INFINITY);
+  if (!ok) {                                              // non-HPD: no NaN/Inf may reach the outputs
+#pragma unroll
+    for (int p = 0; p < U; ++p) w[p] = make_float2(0.f, 0.f);
+  }
   return ok ? sqrtf(r) : 1.f;
 }
 
@@ -872,7 +877,8 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   float2 col[U];
   load_packed_col<U>(Gs, l, a.kappa, col);
   bool ok;
-  const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+  const float dl = Gs[pidx(U, l, l)].x + a.kappa;          // diagonal entry of this lane's column
+  const float beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
   if (a.Wout) {                                   // prepare: cache W = A^{-1} / beta (upper, packed)
     if (active) {

@@ -152,10 +152,12 @@ def test_zf_limit_n0_zero():
 
 
 @pytest.mark.parametrize("mode", ["pd", "fd"])
-def test_non_hpd_flagged_and_zeroed(mode):
+@pytest.mark.parametrize("cfgid", [2, 4])
+def test_non_hpd_flagged_and_zeroed(mode, cfgid):
     """N0 = 0 with a rank-deficient channel on one subcarrier -> flagged, zero output there,
-    other subcarriers unaffected (SPEC S:60, S:241 typed error rather than Inf)."""
-    cfg = CONFIGS[2]
+    other subcarriers unaffected (SPEC S:60, S:241 typed error rather than Inf); cfg 4 takes
+    the tensor-core kernels."""
+    cfg = CONFIGS[cfgid]
     f = frame(cfg, 9)
     f.H[4] = 0
     f.H[4, :, 0] = 1.0
@@ -165,7 +167,10 @@ def test_non_hpd_flagged_and_zeroed(mode):
     keep = [i for i in range(9) if i != 4]
     sub = synth.Frame(H=f.H[keep], s=f.s[keep], idx=f.idx[keep], qam=f.qam)
     xr, *_ = reference(cfg, sub, mode, 0.0)
-    assert rel_l2(x[keep], xr) <= REL_TOL
+    # square FD clusters (S = U) at N0 = 0 are zero-forcing on a 32 x 32 Rayleigh block:
+    # cond(G_c) ~ 1e5-1e7 bounds fp32 accuracy
+    tol = REL_TOL if (mode == "pd" or cfg.S > cfg.U) else 1e-2
+    assert rel_l2(x[keep], xr) <= tol
     # DP_FLAG_SYNC returns the numeric error directly
     with Precoder(9, cfg.B, cfg.U, cfg.K, cfg.C, flags=L.DP_FLAG_SYNC) as pre:
         fn = pre.precode_pd if mode == "pd" else pre.precode_fd
