@@ -20,8 +20,6 @@
 
 #include "dp.h"
 #include "kernels.cuh"
-#include "gram_tc.cuh"
-#include "precode_tc.cuh"
 #include "fd_tc.cuh"
 #include "solve_mw.cuh"
 #include "precode_tc2.cuh"
@@ -324,28 +322,13 @@ int launch_gram_tc2(dp_ctx *c, const Args &b, cudaStream_t st) {
 template <int U, bool PER_CHUNK>
 int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   if constexpr (U == 32) {
-    static const bool v1 = getenv("DP_GRAM_TC1") != nullptr;   // A/B: SIMT-built operand planes
-    if (c->use_tc && !v1 && a.S % 32 == 0) {      // tensor-core Gram, operands straight from TMA
+    if (c->use_tc && a.S % 32 == 0) {             // tensor-core Gram, operands straight from TMA
       Args b = a;                                 // work item = (subcarrier, group)
       if (!PER_CHUNK) {
         b.S = a.Bl;                               // one group: all local antennas
         b.nchunks = 1;
       }
       return (b.S % 64 == 0) ? launch_gram_tc2<64>(c, b, st) : launch_gram_tc2<32>(c, b, st);
-    }
-    if (c->use_tc && a.S % dpk::TCG_TK == 0) {   // tensor-core (tcgen05) Gram
-      Args b = a;                                 // work item = (subcarrier, group)
-      if (!PER_CHUNK) {
-        b.S = a.Bl;                               // one group: all local antennas
-        b.nchunks = 1;
-      }
-      const int n_items = b.n_sc * b.nchunks;
-      const int grid = std::min(n_items, 2 * c->num_sms);
-      auto kern = dpk::gram_tc_kernel;
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::TCG_SMEM));
-      LaunchScope ls(c, DP_KERNEL_GRAM, st);
-      CK(launch_pdl(kern, dim3(grid), dim3(dpk::TCG_THREADS), dpk::TCG_SMEM, st, b));
-      return DP_OK;
     }
   }
   const size_t sm = smem_gram(U, a.Bl, nw);
@@ -396,7 +379,7 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   return DP_OK;
 }
 
-// 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), TCP_ROWS-row x
+// 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), box_rows-row x
 // 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
 int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
@@ -414,24 +397,6 @@ int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtens
                       CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return DP_OK;
-}
-
-// tensor-core precode applies: U = 32, K <= 16, 128-antenna items, 32-antenna z groups
-bool precode_tc_ok(const dp_ctx *c, const Args &a) {
-  static const bool opt_in = getenv("DP_TC_PRECODE") != nullptr;   // experimental (slower than SIMT today)
-  return opt_in && c->use_tc && c->cfg.U == 32 && a.K <= 16 && a.Bl % dpk::TCP_ROWS == 0 && a.S == 32 &&
-         (a.zgroups == 1 || a.zgroups == a.nchunks);
-}
-
-int launch_precode_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
-  CUtensorMap tm;
-  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, dpk::TCP_ROWS, CU_TENSOR_MAP_SWIZZLE_128B));
-  auto kern = dpk::precode_tc_kernel;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::TCP_SMEM));
-  const int n_items = a.n_sc * (a.Bl / dpk::TCP_ROWS);
-  LaunchScope ls(c, DP_KERNEL_PRECODE, st);
-  CK(launch_pdl(kern, dim3(std::min(n_items, c->num_sms)), dim3(dpk::TCP_THREADS), dpk::TCP_SMEM, st, tm, a));
   return DP_OK;
 }
 
@@ -508,11 +473,6 @@ int launch_fd_tc_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
   }
 }
 
-int launch_finish(dp_ctx *c, const Args &a, cudaStream_t st) {
-  LaunchScope ls(c, DP_KERNEL_FINISH, st);
-  CK(launch_pdl(dpk::fd_finish_kernel, dim3((a.n_sc + 127) / 128), dim3(128), 0, st, a));
-  return DP_OK;
-}
 
 // ---------------------------------------------------------------- U / KC dispatch
 template <template <int, int> class F, int U, typename... T>
@@ -780,9 +740,6 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   a.chunks_per_zgroup = c->pd_nchunks;
   if (precode_tc2_ok(c, a)) {
     RET(launch_precode_tc2(c, a, st));               // tensor-core precode, writes the scalars
-  } else if (precode_tc_ok(c, a)) {
-    RET(launch_precode_tc(c, a, st));                // tensor-core precode (+ scalar finish)
-    RET(launch_finish(c, a, st));
   } else {
     RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
   }

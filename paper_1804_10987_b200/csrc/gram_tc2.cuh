@@ -15,8 +15,8 @@
 // an MN-major SWIZZLE_128B_BASE32B operand (M = reals, K = antennas; LBO = CH * 128 B
 // between the 32-real atoms, SBO = 512 B between 4-antenna K groups).  The residual
 // plane Xs is written right behind it in the same layout, so A = [Xb^T; Xs^T] is four
-// equally spaced atoms and B = Xb^T the first two (gram_tc.cuh built both planes with
-// SIMT conversions; here only the residual is computed).
+// equally spaced atoms and B = Xb^T the first two (only the residual plane is computed
+// with SIMT instructions; an earlier version converted both planes).
 //
 // Persistent, warp-specialised, one CTA per SM (10 warps):
 //   warp 8     TMA: CH-antenna chunks into an NS-stage ring (tx-count mbarriers);

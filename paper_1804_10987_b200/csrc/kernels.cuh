@@ -708,6 +708,12 @@ struct Args {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// named barrier over n threads; plain mbarrier arrive (tensor-core kernels' hand-offs)
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(mbar)) : "memory");
+}
+
 // Per-subcarrier scalars in a fixed order over the local parts (read through L2:
 // other CTAs wrote them).
 __device__ __forceinline__ void finish_sc(const Args &a, int sc) {
@@ -766,7 +772,11 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   // stage s_k of this subcarrier into the (now free) T region while the sweep runs
   sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
   bool ok;
-  const float beta = sweep_sg<U>(col, slot, l, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+  float dl = 0.f;                                         // this lane's diagonal entry A[l][l]
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u == l) dl = col[u].x;
+  const float beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;   // sign folds -A^{-1}; failed problems: x = 0
   cp_async_wait_all();
   __syncwarp();
