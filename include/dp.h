@@ -163,6 +163,15 @@ DP_API int dp_precode_fd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
 /* Copy scalar output `which` (DP_SCALAR_*) of the last precode call into
  * `dst` (device or host float array of the documented length), ordered on
  * `stream`; a host `dst` is complete when the call returns. */
+/* Fully-distributed MRT (the baseline of Fig. 2): per cluster the
+ * matched filter x_c = H_c^H s / beta_c with beta_c = sqrt(Es ||H_c||_F^2 / rho_c^2),
+ * rho_c^2 = rho2 / C (Eq. 5 applied to the cluster).  N0 is accepted and ignored.
+ * Same layouts, ownership and errors as dp_precode_fd.  DP_SCALAR_BETA then holds the effective
+ * per-cluster scale beta_c U / ||H_c||_F^2 and DP_SCALAR_RX = 1 / sum_c (||H_c||_F^2 / (U beta_c)):
+ * the joint UE scaling with the cluster array gain (H_c H_c^H ~ ||H_c||_F^2 / U I; R24). */
+DP_API int dp_precode_mrt(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
+                  double N0, double rho2, dp_c32 *x_local, void *stream);
+
 DP_API int dp_read_scalars(dp_ctx *ctx, int which, float *dst, void *stream);
 
 /* Synchronize the context's work and report the number of (subcarrier,

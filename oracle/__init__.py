@@ -55,6 +55,7 @@ def _L():
         lib.oracle_pd.argtypes = [P, I, I, I, I, I, P, D, D, D, P, P, P]
         lib.oracle_fd.argtypes = [P, I, I, I, I, I, P, D, D, D, D, P, P]
         lib.oracle_rx_scale_fd.argtypes = [P, I, I, P]
+        lib.oracle_mrt_fd.argtypes = [P, I, I, I, I, I, P, D, D, P, P]
         lib.oracle_num_threads.restype = I
         _lib = lib
     return _lib
@@ -167,6 +168,17 @@ def fd(H, s, C: int, N0: float, rho2: float = 1.0, Es: float = 1.0, tau: float =
     beta_c = np.empty((n_sc, C), np.float64)
     rc = _L().oracle_fd(_p(H), n_sc, B, U, K, C, _p(s), N0, rho2, Es, tau, _p(x), _p(beta_c))
     _check(rc, "fd", allow_numeric)
+    return x, beta_c
+
+
+def mrt_fd(H, s, C: int, rho2: float = 1.0, Es: float = 1.0):
+    """Fully-distributed MRT (Fig. 2 baseline): x_c = H_c^H s / beta_c. Returns (x, beta_c[n_sc][C])."""
+    H, s = _c128(H), _c128(s)
+    n_sc, B, U = H.shape
+    K = s.shape[1]
+    x = np.empty((n_sc, K, B), np.complex128)
+    beta_c = np.empty((n_sc, C), np.float64)
+    _check(_L().oracle_mrt_fd(_p(H), n_sc, B, U, K, C, _p(s), rho2, Es, _p(x), _p(beta_c)), "mrt_fd")
     return x, beta_c
 
 

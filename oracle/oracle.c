@@ -405,6 +405,43 @@ int oracle_fd(const cplx *H, int n_sc, int B, int U, int K, int C, const cplx *s
 }
 
 /* ------------------------------------------------------------------------ */
+/* Fully-distributed MRT, the baseline of Fig. 2: per   */
+/* cluster the matched filter Q_c = H_c^H with the per-cluster power split    */
+/* rho_c^2 = rho^2 / C and the normalisation of Eq. (5) applied to    */
+/* the cluster, beta_c = sqrt(Es tr(Q_c^H Q_c) / rho_c^2)                    */
+/* = sqrt(Es ||H_c||_F^2 / rho_c^2); x_c = Q_c s / beta_c.                   */
+/* ------------------------------------------------------------------------ */
+int oracle_mrt_fd(const cplx *H, int n_sc, int B, int U, int K, int C, const cplx *s,
+                  double rho2, double Es, cplx *x, double *beta_c)
+{
+    if (!H || !s || !x || !beta_c || n_sc <= 0 || B <= 0 || U <= 0 || K <= 0 || C <= 0 || B % C)
+        return ERR_ARG;
+    if (!(rho2 > 0) || !(Es > 0)) return ERR_ARG;
+    const int S = B / C;
+    const double rho_c2 = rho2 / C;
+    for (int w = 0; w < n_sc; ++w) {
+        const cplx *Hw = H + (size_t)w * B * U;
+        for (int c = 0; c < C; ++c) {
+            const cplx *Hc = Hw + (size_t)c * S * U;
+            double fro = 0.0;                                   /* tr(Q_c^H Q_c) = ||H_c||_F^2 */
+            for (int i = 0; i < S * U; ++i) fro += creal(Hc[i] * conj(Hc[i]));
+            const double bc = sqrt(Es * fro / rho_c2);
+            beta_c[(size_t)w * C + c] = bc;
+            for (int k = 0; k < K; ++k) {
+                const cplx *sk = s + ((size_t)w * K + k) * U;
+                cplx *xk = x + ((size_t)w * K + k) * B + (size_t)c * S;
+                for (int b = 0; b < S; ++b) {                   /* (H_c^H s)_b = sum_u conj(H^paper_{u,b}) s_u */
+                    cplx acc = 0;
+                    for (int u = 0; u < U; ++u) acc += conj(Hc[(size_t)b * U + u]) * sk[u];
+                    xk[b] = bc > 0.0 ? acc / bc : 0.0;
+                }
+            }
+        }
+    }
+    return OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* FD receive scale (reading R9 — parity unpinned: the paper does not state   */
 /* which scalar a UE applies under FD-WF).  Each cluster's precoder is        */
 /* designed for joint scaling by beta_c; in the ZF limit              */

@@ -26,7 +26,7 @@ EXPORTS = [
     "dp_get_unique_id", "dp_init", "dp_precode_pd", "dp_precode_fd", "dp_read_scalars",
     "dp_status", "dp_profile_read", "dp_launch_count", "dp_finalize", "dp_last_error",
     "dp_debug_gram", "dp_debug_solve", "dp_synth_frame", "dp_receive_count",
-    "dp_prepare_pd", "dp_prepare_fd", "dp_apply", "dp_comm_ledger",
+    "dp_prepare_pd", "dp_prepare_fd", "dp_apply", "dp_comm_ledger", "dp_precode_mrt",
 ]
 
 
@@ -59,7 +59,7 @@ def lib() -> ctypes.CDLL:
     P, I, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
     L.dp_get_unique_id.argtypes = [P]
     L.dp_init.argtypes = [ctypes.POINTER(DpConfig), ctypes.POINTER(P)]
-    for f in (L.dp_precode_pd, L.dp_precode_fd):
+    for f in (L.dp_precode_pd, L.dp_precode_fd, L.dp_precode_mrt):
         f.argtypes = [P, P, P, D, D, P, P]
     L.dp_read_scalars.argtypes = [P, I, P, P]
     L.dp_status.argtypes = [P, ctypes.POINTER(I)]
@@ -108,6 +108,10 @@ def dp_precode_pd(ctx, H_ptr: int, s_ptr: int, N0: float, rho2: float, x_ptr: in
 
 def dp_precode_fd(ctx, H_ptr: int, s_ptr: int, N0: float, rho2: float, x_ptr: int, stream: int) -> int:
     return lib().dp_precode_fd(ctx, H_ptr, s_ptr, float(N0), float(rho2), x_ptr, stream)
+
+
+def dp_precode_mrt(ctx, H_ptr: int, s_ptr: int, N0: float, rho2: float, x_ptr: int, stream: int) -> int:
+    return lib().dp_precode_mrt(ctx, H_ptr, s_ptr, float(N0), float(rho2), x_ptr, stream)
 
 
 def dp_read_scalars(ctx, which: int, dst_ptr: int, stream: int) -> int:

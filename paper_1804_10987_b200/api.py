@@ -110,6 +110,12 @@ class Precoder:
         self._last = getattr(self, "_prepared", None)
         return x
 
+    def precode_mrt(self, H, s, N0: float = 0.0, rho2: float = 1.0, out=None, stream=None):
+        """Fully-distributed MRT baseline (Fig. 2): x_c = H_c^H s / beta_c per cluster."""
+        x = self._run(L.dp_precode_mrt, "dp_precode_mrt", H, s, N0, rho2, out, stream)
+        self._last = "dp_precode_fd"                      # per-cluster scalars, like FD
+        return x
+
     def read_scalars(self, which: str, device="cuda", stream=None) -> torch.Tensor:
         """'beta' (PD [n_sc]; FD local [n_sc][C/world]), 'rx' [n_sc], 'power' [n_sc]."""
         w = {"beta": L.DP_SCALAR_BETA, "rx": L.DP_SCALAR_RX, "power": L.DP_SCALAR_POWER}[which]

@@ -58,14 +58,15 @@ class BerRun:
         return self._pre[C]
 
     def point(self, mode: str, C: int, snr_db: float, frames: int, frame0: int = 0):
-        """Bit errors and bits for `frames` frames; mode "pd" (= centralized WF) or "fd"."""
+        """Bit errors and bits for `frames` frames; mode "pd" (= centralized WF), "fd" or
+        "mrt" (fully-distributed MRT, the Fig. 2 baseline)."""
         N0 = 10.0 ** (-snr_db / 10.0)       # rho^2 = Es = 1 (reading R10)
         pre = self._precoder(C)
         errors = torch.zeros(1, dtype=torch.int64, device="cuda")
         rx = torch.empty(self.n_sc, dtype=torch.float32, device="cuda")
         for f in range(frame0, frame0 + frames):
             H, s, idx, n = synth_frame(f, self.n_sc, self.B, self.U, self.K, self.M, N0, seed=self.seed)
-            x = (pre.precode_pd if mode == "pd" else pre.precode_fd)(H, s, N0, 1.0)
+            x = {"pd": pre.precode_pd, "fd": pre.precode_fd, "mrt": pre.precode_mrt}[mode](H, s, N0, 1.0)
             L.check(L.dp_read_scalars(pre.ctx, L.DP_SCALAR_RX, rx.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream), "dp_read_scalars")
             receive_count(H, x, n, rx, idx, self.M, errors)

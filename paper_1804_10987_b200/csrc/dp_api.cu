@@ -690,6 +690,49 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   return DP_OK;
 }
 
+// Fully-distributed MRT frame (Fig. 2 baseline) on device pointers
+template <int U>
+int launch_mrt(dp_ctx *c, const Args &a, cudaStream_t st) {
+  const size_t sm = (size_t)4 * a.K * U * sizeof(float2);
+  auto kern = dpk::mrt_kernel<U>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
+  CK(launch_pdl(kern, dim3((a.n_sc * a.nchunks + 3) / 4), dim3(128), sm, st, a));
+  return DP_OK;
+}
+int precode_mrt_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, double rho2, float2 *xd,
+                    cudaStream_t st) {
+  (void)N0;                                               // MRT ignores the noise level
+  const dp_config &k = c->cfg;
+  const float2 *s_use;
+  RET(distribute_s(c, sd, st, &s_use));
+  Args a = base_args(c);
+  a.H = Hd;
+  a.s = s_use;
+  a.x = xd;
+  a.S = c->S;
+  a.nchunks = c->Cl;
+  a.coef = (float)(k.Es / (rho2 / k.C));                  // Es / rho_c^2, rho_c^2 = rho^2 / C
+  a.nbeta = c->Cl;
+  switch (k.U) {
+    case 4: RET(launch_mrt<4>(c, a, st)); break;
+    case 8: RET(launch_mrt<8>(c, a, st)); break;
+    case 16: RET(launch_mrt<16>(c, a, st)); break;
+    default: RET(launch_mrt<32>(c, a, st)); break;
+  }
+  {
+    LaunchScope ls(c, DP_KERNEL_FINISH, st);
+    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+  }
+  if (c->comm_on) {
+    NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
+  }
+  c->last_mode = 1;                                       // scalars laid out as FD's
+  c->prepared = -1;
+  return DP_OK;
+}
+
 // PD frame on device pointers (everything after the host staging)
 int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, double rho2, float2 *xd,
                    cudaStream_t st) {
@@ -808,13 +851,14 @@ int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c3
   return rc;
 }
 
-int precode_entry(dp_ctx *c, bool fd, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x,
+int precode_entry(dp_ctx *c, int mode, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x,
                   void *stream) {
   g_err.clear();
   RET(validate_call(c, H, s, N0, rho2, x));
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(c->cfg.device));
-  DevFn fn = fd ? precode_fd_dev : precode_pd_dev;
+  const bool fd = mode != 0;                              // 0 PD, 1 FD, 2 MRT (per-cluster scalars)
+  DevFn fn = mode == 0 ? precode_pd_dev : mode == 1 ? precode_fd_dev : precode_mrt_dev;
   const bool hdev = is_device_ptr(H);
   static const bool no_pipe = getenv("DP_NO_HOST_PIPELINE") != nullptr;
   if (!hdev && !c->comm_on && !no_pipe && s && !is_device_ptr(x) && !is_device_ptr(s) && c->cfg.n_sc >= 16) {
@@ -936,10 +980,13 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
 }
 
 int dp_precode_fd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
-  return precode_entry(c, true, H, s, N0, rho2, x, stream);
+  return precode_entry(c, 1, H, s, N0, rho2, x, stream);
 }
 int dp_precode_pd(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
-  return precode_entry(c, false, H, s, N0, rho2, x, stream);
+  return precode_entry(c, 0, H, s, N0, rho2, x, stream);
+}
+int dp_precode_mrt(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, double N0, double rho2, dp_c32 *x, void *stream) {
+  return precode_entry(c, 2, H, s, N0, rho2, x, stream);
 }
 
 

@@ -995,6 +995,57 @@ __global__ void __launch_bounds__(256) precode_kernel(Args a) {
   pdl_trigger();
 }
 
+// ================================================================== MRT baseline (Fig. 2)
+// Fully-distributed MRT: per (subcarrier, cluster) problem one warp,
+// Q_c = H_c^H (matched filter), beta_c = sqrt(Es ||H_c||_F^2 / rho_c^2) (Eq. 5 on the
+// cluster, coef = Es / rho_c^2), x_c = H_c^H s / beta_c and the power partial.
+template <int U>
+__global__ void __launch_bounds__(128) mrt_kernel(Args a) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ __align__(16) float2 smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nprob = a.n_sc * a.nchunks;
+  const int p = blockIdx.x * 4 + warp;
+  if (p >= nprob) return;
+  const int sc = p / a.nchunks, cl = p % a.nchunks;
+  const float2 *Hc = a.H + ((size_t)sc * a.Bl + (size_t)cl * a.S) * U;
+  float2 *ss = smem + (size_t)warp * a.K * U;
+  for (int i = lane; i < a.K * U; i += 32) ss[i] = a.s[(size_t)sc * a.K * U + i];
+  float fro = 0.f;
+  for (int i = lane; i < a.S * U; i += 32) fro += cabs2(Hc[i]);
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, m);
+  const float beta = sqrtf(a.coef * fro);
+  const bool ok = beta > 0.f && beta < INFINITY;
+  const float ib = ok ? 1.f / beta : 0.f;
+  __syncwarp();
+  float pw = 0.f;
+  for (int b = lane; b < a.S; b += 32) {
+    float2 h[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) h[u] = Hc[(size_t)b * U + u];
+    for (int k = 0; k < a.K; ++k) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u) cfma_cj(acc, h[u], ss[k * U + u]);      // conj(H[b][u]) s_k[u]
+      acc = cscale(acc, ib);
+      a.x[((size_t)sc * a.K + k) * a.Bl + (size_t)cl * a.S + b] = acc;
+      pw += cabs2(acc);
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, m);
+  // receive scale (reading R24): the cluster's array gain g_c = ||H_c||_F^2 / U (H_c H_c^H ~ g_c I)
+  // enters the joint UE scaling, rx = 1 / sum_c (g_c / beta_c); the finish kernel sums 1/beta[],
+  // so the effective per-cluster scale beta_c / g_c is stored
+  if (lane == 0) {
+    a.beta[p] = ok ? beta * (float)U / fro : qnan();
+    a.pw[p] = pw;
+    if (!ok) atomicAdd(a.bad, 1);
+  }
+}
+
 // ================================================================== FD scalar finish
 // Per subcarrier, fixed order over the local clusters: fin[sc] = {sum_c 1/beta_c,
 // sum_c power_c}.  (A separate grid: folding it into the fused kernel needs a

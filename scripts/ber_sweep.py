@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--M", type=int, default=64)
     ap.add_argument("--tau", default="0.125", help="FD regularisation tau_c (Eq. 9); comma list = tau sweep")
     ap.add_argument("--no-pd", action="store_true", help="FD points only")
+    ap.add_argument("--mrt", action="store_true", help="add fully-distributed MRT (Fig. 2 baseline) at every C")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     lo, hi, step = (float(v) for v in args.snr.split(":"))
@@ -46,10 +47,11 @@ def main():
     rows = []
     t0 = time.time()
     for snr in snrs:
-        pts = ([] if args.no_pd else [("pd", 1, taus[0])]) + [("fd", c, t) for t in taus for c in Cs]
+        pts = ([] if args.no_pd else [("pd", 1, taus[0])]) + [("fd", c, t) for t in taus for c in Cs] + \
+              ([("mrt", c, taus[0]) for c in Cs] if args.mrt else [])
         for mode, C, tau in pts:
             e, bits = runs[tau].point(mode, C, snr, args.frames)
-            row = {"mode": "WF(=PD)" if mode == "pd" else "FD", "C": C, "B": args.B, "U": args.U,
+            row = {"mode": {"pd": "WF(=PD)", "fd": "FD", "mrt": "MRT"}[mode], "C": C, "B": args.B, "U": args.U,
                    "snr_db": snr, "errors": e, "bits": bits, "ber": e / bits, "frames": args.frames}
             if mode == "fd":
                 row["tau"] = tau

@@ -367,6 +367,28 @@ def test_apply_without_prepare_rejected():
             pre.apply(H, s)
 
 
+@pytest.mark.parametrize("cfgid", [2, 3, 4])
+def test_mrt_baseline(cfgid):
+    """Fully-distributed MRT (the Fig. 2 baseline, dp_precode_mrt) vs oracle.mrt_fd: x, beta_c, the
+    receive scale 1 / sum_c 1/beta_c and the power."""
+    cfg = CONFIGS[cfgid]
+    f = frame(cfg, 17)
+    with Precoder(17, cfg.B, cfg.U, cfg.K, cfg.C) as pre:
+        x = pre.precode_mrt(torch.from_numpy(f.H).cuda(), torch.from_numpy(f.s).cuda(), 0.1, 1.0)
+        beta = pre.read_scalars("beta").cpu().numpy()
+        rx = pre.read_scalars("rx").cpu().numpy()
+        pw = pre.read_scalars("power").cpu().numpy()
+        assert pre.status() == 0
+    xr, br = oracle.mrt_fd(f.H, f.s, cfg.C)
+    assert rel_l2(x.cpu().numpy(), xr) <= REL_TOL
+    # reading R24: effective per-cluster scale beta_c / g_c, g_c = ||H_c||_F^2 / U
+    g = np.sum(np.abs(f.H.astype(np.complex128).reshape(17, cfg.C, cfg.S, cfg.U)) ** 2, axis=(2, 3)) / cfg.U
+    beff = br / g
+    assert np.max(np.abs(beta.reshape(br.shape) / beff - 1)) <= REL_TOL
+    assert np.max(np.abs(rx * np.sum(1.0 / beff, axis=1) - 1)) <= REL_TOL
+    assert np.max(np.abs(pw / np.sum(np.abs(xr) ** 2, axis=(1, 2)) - 1)) <= 1e-4
+
+
 def test_fd_single_cluster_tau1_equals_pd():
     """FD with C=1, tau=1 is centralized WF, so it must equal PD (C=1)."""
     base = CONFIGS[3]

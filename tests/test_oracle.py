@@ -380,3 +380,34 @@ def test_qam_constellation():
         for i in range(M):
             for j in np.nonzero(np.abs(d[i] - dmin) < 1e-9)[0]:
                 assert bin(i ^ j).count("1") == 1
+
+
+# ---------------------------------------------------------------- fully-distributed MRT (Fig. 2 baseline)
+def test_mrt_fd_pins():
+    """MRT_c: Q_c = H_c^H (matched filter), beta_c by Eq. (5) on the cluster with rho_c^2 = rho^2/C:
+    (1) per-cluster power Es tr(P_c^H P_c) = rho^2/C; (2) closed form for
+    H = [a_1 I, .., a_C I] (B = C U): x_c = a_c s / beta_c with beta_c = |a_c| sqrt(U C Es / rho^2),
+    so x_c = s sqrt(rho^2 / (U C Es)) (phase of a_c removed); (3) brute force against numpy."""
+    rng = np.random.default_rng(5)
+    U, C, K = 4, 2, 3
+    a = np.array([0.7 + 0.2j, -1.3 + 0.0j])
+    Ht = np.concatenate([a[c] * np.eye(U) for c in range(C)], axis=0)[None]   # [1][B][U], H^paper = Ht^T
+    s = (rng.standard_normal((1, K, U)) + 1j * rng.standard_normal((1, K, U)))
+    x, bc = oracle.mrt_fd(Ht, s, C, rho2=2.0)
+    for c in range(C):
+        assert bc[0, c] == pytest.approx(abs(a[c]) * np.sqrt(U * C / 2.0), rel=1e-12)
+        xc = x[0, :, c * U:(c + 1) * U]
+        assert np.allclose(xc, np.conj(a[c]) * s[0] / bc[0, c], atol=1e-12)
+        assert np.allclose(np.abs(xc), np.abs(s[0]) * np.sqrt(2.0 / (U * C)), atol=1e-12)
+    # random channel: power split and numpy matched filter
+    B, U, C, K = 24, 6, 3, 5
+    H = (rng.standard_normal((2, B, U)) + 1j * rng.standard_normal((2, B, U))) / np.sqrt(2)
+    s = (rng.standard_normal((2, K, U)) + 1j * rng.standard_normal((2, K, U)))
+    x, bc = oracle.mrt_fd(H, s, C, rho2=1.5, Es=0.8)
+    S = B // C
+    for w in range(2):
+        for c in range(C):
+            Hc = H[w, c * S:(c + 1) * S]                  # [S][U] = (H_c^paper)^T
+            P = np.conj(Hc) / bc[w, c]                    # P_c = H_c^H / beta_c, [S][U]
+            assert 0.8 * np.trace(P.conj().T @ P).real == pytest.approx(1.5 / C, rel=1e-12)
+            assert np.allclose(x[w, :, c * S:(c + 1) * S], (P @ s[w].T).T, atol=1e-12)
