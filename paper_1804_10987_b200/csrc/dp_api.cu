@@ -563,8 +563,6 @@ Args base_args(dp_ctx *c) {
   a.bad = c->bad;
   a.fin = c->fin;
   a.fin_inv_beta = 1;
-  static const int dbg = getenv("DP_DBG") ? atoi(getenv("DP_DBG")) : 0;
-  a.dbg = dbg;
   return a;
 }
 

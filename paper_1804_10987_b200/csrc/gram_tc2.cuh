@@ -101,12 +101,10 @@ __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __g
           tc::mbar_wait(&prep_done[s], ph);
           tc::fence_after_sync();
           const uint32_t base = tc::smem_u32(sm + (size_t)s * T::STAGE);
-          if (!(a.dbg & 1)) {
 #pragma unroll
           for (int t = 0; t < CH / 8; ++t) {                 // antennas 8t .. 8t+7
             const uint64_t dsc = smem_desc_mn_sw128b32(base + 1024 * t, T::BOX, 512);
             tc::mma_tf32(d, dsc, dsc, IDESC, (c > 0 || t > 0) ? 1u : 0u);
-          }
           }
           tc::mma_commit(&stage_free[s]);
           if (++s == T::NS) { s = 0; ph ^= 1; }
@@ -126,7 +124,6 @@ __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __g
         uint4 *dst = reinterpret_cast<uint4 *>(st + 2 * T::BOX);
         constexpr int NV = 2 * T::BOX / 16 / 128;
         uint4 v[NV];
-        if (!(a.dbg & 2)) {
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = src[ptid + 128 * i];
 #pragma unroll
@@ -137,7 +134,6 @@ __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __g
           f.z = __uint_as_float(v[i].z) - __uint_as_float(v[i].z & 0xFFFFE000u);
           f.w = __uint_as_float(v[i].w) - __uint_as_float(v[i].w & 0xFFFFE000u);
           dst[ptid + 128 * i] = *reinterpret_cast<uint4 *>(&f);
-        }
         }
         tc::fence_proxy_async();
         mbar_arrive(&prep_done[s]);

@@ -699,7 +699,6 @@ struct Args {
   int nbeta;            // beta entries per subcarrier: PD 1, FD clusters per rank
   int fin_inv_beta;     // 1: fin[.][0] = sum 1/beta ; 0: fin[.][0] = 0 (PD ranks != 0)
   int pf_dist;          // fd_tc: L2-prefetch the tiles of CTA blockIdx.x + pf_dist (0: off)
-  int dbg;              // experiment switches (env DP_DBG; 0 in production)
   int fold;             // fd_tc: per-subcarrier scalars in-kernel (CTAs per subcarrier; 0 = finish kernel)
 };
 
