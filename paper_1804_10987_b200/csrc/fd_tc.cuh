@@ -63,34 +63,11 @@ __device__ __forceinline__ float4 ld_chunk_sw128(const uint8_t *tile, int r, int
                                            ((cp & 1) << 4));
 }
 
-// Whitening with the symbols innermost (K <= 16, one chunk of KC):
-//   z_k[l] = ib * sum_v conj(d[v]) s_k[v],  d = column l of -A^{-1} (Hermitian), ib = -1/beta,
-// for all k at once: per v one conj(d[v]) multiplier feeds KC independent accumulators
-// (no long dependent FMA chains), s read from a transposed copy sT[v][k] (row stride
-// FDT_SP complex, broadcast loads).  z is written as zT[u][k] (row stride FDT_SP).
-constexpr int FDT_SP = 18;    // sT / zT row stride (complex): 144 B rows, 16-byte aligned, spread banks
+// z rows of the FD kernel: the symbols-innermost whitening of kernels.cuh (whiten_Tg)
+constexpr int FDT_SP = WT_SP;
 template <int KC>
 __device__ __forceinline__ void whiten_T(const float2 (&d)[32], float ib, const float2 *sT, float2 *zT, int K, int l) {
-  constexpr int KP = (KC + 1) & ~1;
-  float2 acc[KP];
-#pragma unroll
-  for (int j = 0; j < KP; ++j) acc[j] = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int v = 0; v < 32; ++v) {
-    const float4 *row = reinterpret_cast<const float4 *>(sT + v * FDT_SP);
-#pragma unroll
-    for (int j = 0; j < KP; j += 2) {
-      const float4 sv = row[j >> 1];
-      cfma_cj(acc[j], d[v], lo2(sv));
-      cfma_cj(acc[j + 1], d[v], hi2(sv));
-    }
-  }
-  float4 *zo = reinterpret_cast<float4 *>(zT + l * FDT_SP);
-#pragma unroll
-  for (int j = 0; j < KP; j += 2) {
-    const float a0 = j < K ? ib : 0.f, a1 = j + 1 < K ? ib : 0.f;
-    zo[j >> 1] = make_float4(acc[j].x * a0, acc[j].y * a0, acc[j + 1].x * a1, acc[j + 1].y * a1);
-  }
+  whiten_Tg<32, KC>(d, ib, sT, zT, K, l);
 }
 
 // x[k][r] = sum_u conj(H[r][u]) z[k][u] for the lane's row r = l (S = U = 32)

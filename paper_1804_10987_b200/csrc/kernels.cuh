@@ -117,6 +117,10 @@ __device__ __forceinline__ void sg_copy_async(float2 *dst, const float2 *__restr
   for (int i = l; i < n / 2; i += U) cp_async16(dst + 2 * i, src + 2 * i);
 }
 
+// row stride (complex) of the transposed s and of z in the symbols-innermost whitening
+// (whiten_Tg): 144-byte rows, 16-byte aligned, spread over the banks
+constexpr int WT_SP = 18;
+
 // ------------------------------------------------------------------ z layout
 // zT[u][k] with symbols grouped in chunks of KC, each chunk starting at an even
 // (16-byte aligned) offset: index(u, k) = u*zs + (k/KC)*KCP + k%KC.
@@ -293,7 +297,9 @@ template <int U> struct Scr {
 // stalls in the whitening loop.)
 template <int U, int KC>
 __host__ __device__ inline int fd_scr_size(int K) {
-  const int m1 = (U / 2) * (U / 2 + 2), m2 = K * U + U * ZL<KC>::zs(K);
+  const int m1 = (U / 2) * (U / 2 + 2);
+  const int m2 = K <= 16 ? (K * U > U * WT_SP ? K * U : U * WT_SP) + U * WT_SP   // ss|zT, sT (whiten_Tg)
+                         : K * U + U * ZL<KC>::zs(K);
   return 2 * U + (m1 > m2 ? m1 : m2);
 }
 // solve kernel scratch per SG: [slot 2U][packed G][s K x U][zT U x zs]
@@ -625,14 +631,55 @@ __device__ __forceinline__ void whiten_sg(const float2 (&d)[U], float ib, const 
   }
 }
 
+// Whitening with the symbols innermost (K <= 16, one chunk of KC) for an SG of U lanes:
+//   z_k[l] = ib * sum_v conj(d[v]) s_k[v],  d = column l of -A^{-1} (Hermitian), ib = -1/beta,
+// for all k at once: per v one conj(d[v]) multiplier feeds KC independent accumulators (no long
+// dependent FMA chains); s read from a transposed copy sT[v][k] (row stride WT_SP complex,
+// broadcast loads within the SG); z written as zT[u][k] (row stride WT_SP).
+template <int U, int KC>
+__device__ __forceinline__ void whiten_Tg(const float2 (&d)[U], float ib, const float2 *sT, float2 *zT, int K, int l) {
+  constexpr int KP = (KC + 1) & ~1;
+  float2 acc[KP];
+#pragma unroll
+  for (int j = 0; j < KP; ++j) acc[j] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int v = 0; v < U; ++v) {
+    const float4 *row = reinterpret_cast<const float4 *>(sT + v * WT_SP);
+#pragma unroll
+    for (int j = 0; j < KP; j += 2) {
+      const float4 sv = row[j >> 1];
+      cfma_cj(acc[j], d[v], lo2(sv));
+      cfma_cj(acc[j + 1], d[v], hi2(sv));
+    }
+  }
+  float4 *zo = reinterpret_cast<float4 *>(zT + l * WT_SP);
+#pragma unroll
+  for (int j = 0; j < KP; j += 2) {
+    const float a0 = j < K ? ib : 0.f, a1 = j + 1 < K ? ib : 0.f;
+    zo[j >> 1] = make_float4(acc[j].x * a0, acc[j].y * a0, acc[j + 1].x * a1, acc[j + 1].y * a1);
+  }
+}
+// sT[l][k] = s_k[l] (lane l of the SG writes its row; zero padded to KP) from ss [K][U]
+template <int U, int KC>
+__device__ __forceinline__ void transpose_s(const float2 *ss, float2 *sT, int K, int l) {
+  constexpr int KP = (KC + 1) & ~1;
+  float4 *row = reinterpret_cast<float4 *>(sT + l * WT_SP);
+#pragma unroll
+  for (int j = 0; j < KP; j += 2) {
+    const float2 s0 = j < K ? ss[j * U + l] : make_float2(0.f, 0.f);
+    const float2 s1 = j + 1 < K ? ss[(j + 1) * U + l] : make_float2(0.f, 0.f);
+    row[j >> 1] = make_float4(s0.x, s0.y, s1.x, s1.y);
+  }
+}
+
 // ------------------------------------------------------------------ (c) precode
 // x[k][r] = sum_u conj(H[row0 + r][u]) z[k][u] for r = l, l+U, ... < nrows.
 // Writes x[k * xstride + r]; returns the lane's sum of |x|^2.
 template <int U, int KC>
 __device__ __forceinline__ float precode_sg(const float2 *tile, int row0, int nrows, const float2 *zT, int K,
-                                            float2 *__restrict__ x, size_t xstride, int l) {
+                                            float2 *__restrict__ x, size_t xstride, int l, int zs_ = 0) {
   constexpr int KCP = ZL<KC>::KCP;
-  const int zs = ZL<KC>::zs(K);
+  const int zs = zs_ ? zs_ : ZL<KC>::zs(K);
   float pw = 0.f;
   for (int r = l; r < nrows; r += U) {
     const int b = row0 + r;
@@ -779,12 +826,22 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;   // sign folds -A^{-1}; failed problems: x = 0
   cp_async_wait_all();
   __syncwarp();
-  whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  int zs = 0;                                             // zT row stride for the precode
+  if (a.K <= 16) {                                        // symbols innermost over a transposed s
+    float2 *sT = ss + (a.K * U > U * WT_SP ? a.K * U : U * WT_SP);
+    transpose_s<U, KC>(ss, sT, a.K, l);
+    __syncwarp();
+    zT = ss;                                              // ss is dead after the transpose
+    whiten_Tg<U, KC>(col, ib, sT, zT, a.K, l);
+    zs = WT_SP;
+  } else {
+    whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  }
   __syncwarp();
   float pw = 0.f;
   if (active)
     pw = precode_sg<U, KC>(tile, 0, a.S, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
-                           (size_t)a.Bl, l);
+                           (size_t)a.Bl, l, zs);
   pw = sg_sum<U>(pw);
   if (active && l == 0) {
     a.beta[p] = ok ? beta : qnan();
