@@ -305,6 +305,8 @@ __host__ __device__ inline int fd_scr_size(int K) {
 // solve kernel scratch per SG: [slot 2U][packed G][s K x U][zT U x zs]
 template <int U, int KC>
 __host__ __device__ inline int solve_scr_size(int K) {
+  if (K <= 16)                                            // ss | zT, sT (whiten_Tg)
+    return 2 * U + U * (U + 1) / 2 + (K * U > U * WT_SP ? K * U : U * WT_SP) + U * WT_SP;
   return 2 * U + U * (U + 1) / 2 + K * U + U * ZL<KC>::zs(K);
 }
 
@@ -960,11 +962,19 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
     return;
   }
   __syncwarp();
-  whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  if (a.K <= 16) {                                        // symbols innermost over a transposed s
+    float2 *sT = ss + (a.K * U > U * WT_SP ? a.K * U : U * WT_SP);
+    transpose_s<U, KC>(ss, sT, a.K, l);
+    __syncwarp();
+    zT = ss;
+    whiten_Tg<U, KC>(col, ib, sT, zT, a.K, l);
+  } else {
+    whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
+  }
   __syncwarp();
   if (!active) return;
   float2 *zo = a.zout + (size_t)p * a.K * U;
-  for (int k = 0; k < a.K; ++k) zo[(size_t)k * U + l] = zT[ZL<KC>::idx(zs, l, k)];
+  for (int k = 0; k < a.K; ++k) zo[(size_t)k * U + l] = zT[a.K <= 16 ? l * WT_SP + k : ZL<KC>::idx(zs, l, k)];
   if (l == 0) {
     a.beta[p] = ok ? beta : qnan();
     if (!ok) atomicAdd(a.bad, 1);
