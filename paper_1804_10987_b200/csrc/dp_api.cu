@@ -672,9 +672,16 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
     RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
   } else {
     const bool tc = fd_tc_ok(c, a);
+    // SIMT kernel: fold the scalars when every CTA holds whole subcarriers
+    const int nsg = c->fd_nw * (32 / k.U);
+    const bool simt_fold = !tc && nsg <= 32 && nsg % c->Cl == 0 && getenv("DP_NO_FOLD") == nullptr;
     if (tc) RET(launch_fd_tc_kc(c, a, st));
-    else RET(dispatch<FdFused>(k.U, k.K, c, a, st));
-    if (!tc || fd_fold_of(c, a) == 0) {                       // scalars not folded into the kernel
+    else {
+      a.fold = simt_fold ? 1 : 0;
+      RET(dispatch<FdFused>(k.U, k.K, c, a, st));
+      a.fold = 0;
+    }
+    if ((tc && fd_fold_of(c, a) == 0) || (!tc && !simt_fold)) {   // scalars not folded into the kernel
       LaunchScope ls(c, DP_KERNEL_FINISH, st);
       CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
     }

@@ -850,6 +850,24 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
     a.pw[p] = pw;
     if (!ok) atomicAdd(a.bad, 1);
   }
+  if (a.fold) {
+    // the CTA's NSG problems are whole subcarriers (NSG % nchunks == 0): per-subcarrier scalars
+    // here, in the order of finish_sc (ascending cluster), instead of fd_finish_kernel
+    __shared__ float fb[32], fp[32];
+    if (l == 0) { fb[sg] = 1.f / (ok ? beta : qnan()); fp[sg] = pw; }
+    __syncthreads();
+    const int per = NSG / a.nchunks;
+    if ((int)threadIdx.x < per) {
+      const int q0 = threadIdx.x * a.nchunks;
+      if (p0 + q0 < nprob) {
+        const int sc0 = (p0 + q0) / a.nchunks;
+        float b = 0.f, w = 0.f;
+        for (int c = 0; c < a.nchunks; ++c) { b += fb[q0 + c]; w += fp[q0 + c]; }
+        a.fin[2 * sc0] = a.fin_inv_beta ? b : 0.f;
+        a.fin[2 * sc0 + 1] = w;
+      }
+    }
+  }
   pdl_trigger();
 }
 
