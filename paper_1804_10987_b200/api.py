@@ -44,6 +44,7 @@ class Precoder:
         self.cfg = cfg
         self.ctx = L.dp_init(cfg)
         self._last = None
+        self._raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
     # ------------------------------------------------------------ helpers
     def _check_io(self, H, s, x):
@@ -63,6 +64,8 @@ class Precoder:
     def _stream(self, stream):
         if stream is not None:
             return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        if self._raw_stream is not None:
+            return self._raw_stream(self.device)          # torch's current stream, no Stream object
         if torch.cuda.is_available():
             return torch.cuda.current_stream(self.device).cuda_stream
         return 0

@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "dp.h"
@@ -95,6 +97,11 @@ struct dp_ctx {
   // host staging (host-pointer calls)
   float2 *h_dev = nullptr, *s_dev = nullptr, *x_dev = nullptr;
   cudaStream_t st_h2d = nullptr, st_d2h = nullptr;   // host-pointer pipeline copy streams
+  // host-side caches (per-frame host overhead): tensor maps by (pointer, rows, box, swizzle),
+  // device-ness of recently seen pointers
+  struct TmapEntry { const void *p; int rows, box, sw; CUtensorMap tm; };
+  std::vector<TmapEntry> tmaps;
+  std::vector<std::pair<const void *, bool>> ptr_kind;
   // last call
   int last_mode = -1;        // 0 pd, 1 fd
   int prepared = -1;         // W cached in G by dp_prepare_pd (0) / dp_prepare_fd (1); -1 none
@@ -218,6 +225,20 @@ int drain_profile(dp_ctx *c) {
 // ---------------------------------------------------------------- kernel launchers
 using dpk::Args;
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size (host overhead
+// per frame matters when a rank's share of the frame is small, e.g. 8 GPUs)
+template <typename Kern>
+cudaError_t set_smem(Kern kern, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void *, size_t> done;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find((const void *)kern);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[(const void *)kern] = bytes;
+  return e;
+}
+
 // Launch with programmatic dependent launch (PDL): the kernel may be scheduled while
 // its predecessor on the stream drains; every kernel starts with griddepcontrol.wait.
 template <typename Kern, typename... KArgs>
@@ -265,7 +286,7 @@ int launch_fd_small_t(dp_ctx *c, const Args &a, cudaStream_t st) {
   const size_t sm = (size_t)NSG * dpk::fds_size<S, U, KC>(a.K) * sizeof(float2);
   if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "FD small-cluster tiles need %zu B of shared memory", sm);
   auto kern = dpk::fd_small_kernel<S, U, KC>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(kern, sm));
   const int nprob = a.n_sc * a.nchunks;
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
   CK(launch_pdl(kern, dim3((nprob + NSG - 1) / NSG), dim3(128), sm, st, a));
@@ -299,21 +320,21 @@ int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
   const size_t sm = smem_fd_fused(U, a.S, a.K, nw) + pad;
   auto kern = dpk::fd_fused_kernel<U, KC>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(kern, sm));
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
   CK(launch_pdl(kern, dim3((nprob + nsg - 1) / nsg), dim3(nw * 32), sm, st, a));
   return DP_OK;
 }
 
-int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw);
+int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw);
 
 template <int CH>
 int launch_gram_tc2(dp_ctx *c, const Args &b, cudaStream_t st) {
   using T = dpk::GT2<CH>;
   CUtensorMap tm;
-  RET(make_h_tmap(b.H, b.n_sc * b.Bl, &tm, CH, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  RET(make_h_tmap(c, b.H, b.n_sc * b.Bl, &tm, CH, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   auto kern = dpk::gram_tc2_kernel<CH>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
+  CK(set_smem(kern, T::SMEM));
   LaunchScope ls(c, DP_KERNEL_GRAM, st);
   CK(launch_pdl(kern, dim3(std::min(b.n_sc * b.nchunks, c->num_sms)), dim3(T::THREADS), T::SMEM, st, tm, b));
   return DP_OK;
@@ -334,7 +355,7 @@ int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   const size_t sm = smem_gram(U, a.Bl, nw);
   if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "Gram tile needs %zu B of shared memory", sm);
   auto kern = dpk::gram_kernel<U, PER_CHUNK>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(kern, sm));
   LaunchScope ls(c, DP_KERNEL_GRAM, st);
   CK(launch_pdl(kern, dim3(a.n_sc), dim3(nw * 32), sm, st, a));
   return DP_OK;
@@ -350,7 +371,7 @@ int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
       const int NW = nw_env == 2 ? 2 : 4;
       const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KC, NW) * sizeof(float2);
       auto kern = NW == 4 ? dpk::solve_mw_kernel<KC, 4> : dpk::solve_mw_kernel<KC, 2>;
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CK(set_smem(kern, sm));
       LaunchScope ls(c, DP_KERNEL_SOLVE, st);
       CK(launch_pdl(kern, dim3((nprob + 4 / NW - 1) / (4 / NW)), dim3(dpk::SMW_THREADS), sm, st, a));
       return DP_OK;
@@ -362,7 +383,7 @@ int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int per = wpc * (32 / U);
   const size_t sm = smem_solve(U, a.K) / 4 * wpc;
   auto kern = dpk::solve_kernel<U, KC>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(kern, sm));
   LaunchScope ls(c, DP_KERNEL_SOLVE, st);
   CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(32 * wpc), sm, st, a));
   return DP_OK;
@@ -373,7 +394,7 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
   const size_t sm = smem_precode(U, a.Bl, a.K, a.zgroups);
   if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "precode tile needs %zu B of shared memory", sm);
   auto kern = dpk::precode_kernel<U, KC>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(kern, sm));
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
   CK(launch_pdl(kern, dim3(a.n_sc), dim3(nw * 32), sm, st, a));
   return DP_OK;
@@ -381,7 +402,7 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
 
 // 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), box_rows-row x
 // 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
-int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw) {
+int encode_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -400,6 +421,18 @@ int make_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtens
   return DP_OK;
 }
 
+int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw) {
+  for (const auto &e : c->tmaps)
+    if (e.p == H && e.rows == rows && e.box == box_rows && e.sw == (int)sw) {
+      *tm = e.tm;
+      return DP_OK;
+    }
+  RET(encode_h_tmap(H, rows, tm, box_rows, sw));
+  if (c->tmaps.size() >= 16) c->tmaps.erase(c->tmaps.begin());
+  c->tmaps.push_back({H, rows, box_rows, (int)sw, *tm});
+  return DP_OK;
+}
+
 // PD precode on the tensor cores (precode_tc2.cuh): U = 32, one z per subcarrier,
 // K <= 16, 128-antenna blocks
 bool precode_tc2_ok(const dp_ctx *c, const Args &a) {
@@ -409,9 +442,9 @@ bool precode_tc2_ok(const dp_ctx *c, const Args &a) {
 
 int launch_precode_tc2(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
-  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, dpk::PC2_ROWS, CU_TENSOR_MAP_SWIZZLE_128B));
+  RET(make_h_tmap(c, a.H, a.n_sc * a.Bl, &tm, dpk::PC2_ROWS, CU_TENSOR_MAP_SWIZZLE_128B));
   auto kern = dpk::precode_tc2_kernel;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dpk::PC2_SMEM));
+  CK(set_smem(kern, dpk::PC2_SMEM));
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
   CK(launch_pdl(kern, dim3(std::min(a.n_sc, c->num_sms)), dim3(dpk::PC2_THREADS), dpk::PC2_SMEM, st, tm, a));
   return DP_OK;
@@ -438,11 +471,11 @@ int fd_fold_of(const dp_ctx *c, const Args &a) {
 template <int KC, bool WTC>
 int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
-  RET(make_h_tmap(a.H, a.n_sc * a.Bl, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  RET(make_h_tmap(c, a.H, a.n_sc * a.Bl, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   auto kern = dpk::fd_tc_kernel<KC, WTC>;
   static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
   const size_t smem = dpk::FDT_SMEM + pad;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(set_smem(kern, smem));
   const int nprob = a.n_sc * a.nchunks;
   Args b = a;
   b.pf_dist = 3 * c->num_sms;                                // resident CTAs: 3 per SM
@@ -513,7 +546,7 @@ int launch_whiten(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int per = 4 * (32 / U);
   const size_t sm = (size_t)per * (dpk::npacked(U) + a.K * U + U * dpk::ZL<KC>::zs(a.K)) * sizeof(float2);
   auto kern = dpk::whiten_kernel<U, KC>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(kern, sm));
   LaunchScope ls(c, DP_KERNEL_SOLVE, st);
   CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(128), sm, st, a));
   return DP_OK;
@@ -540,6 +573,15 @@ bool is_device_ptr(const void *p) {
     return false;
   }
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+// cached per context (an address does not change between device and host memory under UVA)
+bool is_device_ptr(dp_ctx *c, const void *p) {
+  for (const auto &e : c->ptr_kind)
+    if (e.first == p) return e.second;
+  const bool d = is_device_ptr(p);
+  if (c->ptr_kind.size() >= 64) c->ptr_kind.erase(c->ptr_kind.begin());
+  c->ptr_kind.push_back({p, d});
+  return d;
 }
 
 int validate_call(dp_ctx *c, const void *H, const void *s, double N0, double rho2, void *x) {
@@ -569,8 +611,8 @@ Args base_args(dp_ctx *c) {
 // Stage host pointers into device buffers (H2D on st).  Returns device views.
 int stage_in(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, dp_c32 *x, cudaStream_t st, bool *host,
              const float2 **Hd, const float2 **sd, float2 **xd) {
-  const bool hdev = is_device_ptr(H), xdev = is_device_ptr(x);
-  const bool sdev = s ? is_device_ptr(s) : hdev;
+  const bool hdev = is_device_ptr(c, H), xdev = is_device_ptr(c, x);
+  const bool sdev = s ? is_device_ptr(c, s) : hdev;
   if (hdev != xdev || hdev != sdev)
     return fail(DP_ERR_INVALID, "H_local, s and x_local must all be device pointers or all host pointers");
   *host = !hdev;
@@ -700,7 +742,7 @@ template <int U>
 int launch_mrt(dp_ctx *c, const Args &a, cudaStream_t st) {
   const size_t sm = (size_t)4 * a.K * U * sizeof(float2);
   auto kern = dpk::mrt_kernel<U>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(kern, sm));
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
   CK(launch_pdl(kern, dim3((a.n_sc * a.nchunks + 3) / 4), dim3(128), sm, st, a));
   return DP_OK;
@@ -864,9 +906,9 @@ int precode_entry(dp_ctx *c, int mode, const dp_c32 *H, const dp_c32 *s, double 
   CK(cudaSetDevice(c->cfg.device));
   const bool fd = mode != 0;                              // 0 PD, 1 FD, 2 MRT (per-cluster scalars)
   DevFn fn = mode == 0 ? precode_pd_dev : mode == 1 ? precode_fd_dev : precode_mrt_dev;
-  const bool hdev = is_device_ptr(H);
+  const bool hdev = is_device_ptr(c, H);
   static const bool no_pipe = getenv("DP_NO_HOST_PIPELINE") != nullptr;
-  if (!hdev && !c->comm_on && !no_pipe && s && !is_device_ptr(x) && !is_device_ptr(s) && c->cfg.n_sc >= 16) {
+  if (!hdev && !c->comm_on && !no_pipe && s && !is_device_ptr(c, x) && !is_device_ptr(c, s) && c->cfg.n_sc >= 16) {
     RET(host_pipelined(c, fn, fd ? c->Cl : 1, H, s, N0, rho2, x, st));
     return finish_call(c, false, x, st);                    // numeric check (DP_FLAG_SYNC); data already home
   }
@@ -1300,7 +1342,7 @@ int dp_receive_count(int n_sc, int B, int U, int K, int M, const dp_c32 *H, cons
   a.idx = idx;
   a.errors = errors;
   const size_t sm = ((size_t)B * U + (size_t)K * B) * sizeof(float2);
-  CK(cudaFuncSetAttribute(dpk::rx_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(set_smem(dpk::rx_count_kernel, sm));
   dpk::rx_count_kernel<<<n_sc, 256, sm, (cudaStream_t)stream>>>(a);
   CK(cudaGetLastError());
   return DP_OK;
