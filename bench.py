@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="both", choices=["both", "pd", "fd"])
     ap.add_argument("--unfused", action="store_true", help="three-kernel path (a)(b)(c)")
-    ap.add_argument("--pd-topology", default="allreduce", choices=["allreduce", "reduce_bcast"])
+    ap.add_argument("--pd-topology", default="scatter_gather", choices=["allreduce", "reduce_bcast", "scatter_gather"],
+                    help="PD exchange for N > 1 (DESIGN.md §6); scatter_gather splits the solve over the GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time for cpu_baseline")

@@ -90,6 +90,8 @@ extern "C" {
 #define DP_PD_ALLREDUCE     0  /* allreduce packed G; every rank solves redundantly (default)          */
 #define DP_PD_REDUCE_BCAST  1  /* paper's design: reduce G to rank 0, rank 0 solves
                                   and whitens, broadcast z                                             */
+#define DP_PD_SCATTER_GATHER 2 /* reduce-scatter G over subcarrier blocks, each rank solves and whitens
+                                  its n_sc/world subcarriers, all-gather z and beta (n_sc % world == 0)  */
 
 typedef struct { float re, im; } dp_c32;
 typedef struct dp_ctx dp_ctx;                       /* opaque */
@@ -106,7 +108,7 @@ typedef struct {
                             all ranks; NULL iff world == 1 (without DP_FLAG_FORCE_COMM)         */
     double Es;           /* average symbol energy of the constellation (reading R1), > 0 */
     double tau;          /* FD regularisation scale tau_c (Eq. 9; P:241 default 0.125), >= 0    */
-    int pd_topology;     /* DP_PD_ALLREDUCE or DP_PD_REDUCE_BCAST                               */
+    int pd_topology;     /* DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST or DP_PD_SCATTER_GATHER          */
     int s_on_all_ranks;  /* 1: s is valid on every rank; 0: s is read on rank 0 only and
                             broadcast by the library ("s is the only signal that must be
                             broadcast")                                    */

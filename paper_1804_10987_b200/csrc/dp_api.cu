@@ -796,6 +796,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   a.nbeta = 1;
   a.fin_inv_beta = (k.rank == 0) ? 1 : 0;   // 1/beta contributed once to the scalar allreduce
   const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
+  const bool topo_t3 = c->comm_on && k.pd_topology == DP_PD_SCATTER_GATHER;
   const float2 *s_use = sd;
   if (!topo_t1) RET(distribute_s(c, sd, st, &s_use));   // T2: overlaps nothing yet; only s crosses
   a.s = s_use;
@@ -805,7 +806,27 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
   a.G = c->G;
   a.zout = c->z;
-  if (c->comm_on && !topo_t1) {
+  if (topo_t3) {
+    // subcarrier-split whitening node: rank r receives sum_c G_c of its n_sc/world subcarriers
+    // (reduce-scatter, in place), solves and whitens them, and the z / beta blocks are
+    // all-gathered: the solve scales with the GPU count instead of running on every rank
+    const int nb = k.n_sc / k.world, sc0 = k.rank * nb;
+    const size_t blkG = (size_t)nb * dpk::npacked(k.U) * 2, blkZ = (size_t)nb * k.K * k.U * 2;
+    NK(ncclReduceScatter(c->G, c->G + (size_t)sc0 * dpk::npacked(k.U), blkG, ncclFloat, ncclSum, c->comm, st));
+    LEDGER(c, DP_COMM_GRAM, nG);
+    Args b = a;
+    b.n_sc = nb;
+    b.G = c->G + (size_t)sc0 * dpk::npacked(k.U);
+    b.s = s_use + (size_t)sc0 * k.K * k.U;
+    b.zout = c->z + (size_t)sc0 * k.K * k.U;
+    b.beta = c->beta + sc0;
+    RET(dispatch<Solve>(k.U, k.K, c, b, st));
+    NK(ncclGroupStart());
+    NK(ncclAllGather(c->z + (size_t)sc0 * k.K * k.U, c->z, blkZ, ncclFloat, c->comm, st));
+    NK(ncclAllGather(c->beta + sc0, c->beta, (size_t)nb, ncclFloat, c->comm, st));
+    NK(ncclGroupEnd());
+    LEDGER(c, DP_COMM_Z_BCAST, blkZ + (size_t)nb);
+  } else if (c->comm_on && !topo_t1) {
     // cross-rank adder tree on every rank; every rank whitens redundantly
     NK(ncclAllReduce(c->G, c->G, nG, ncclFloat, ncclSum, c->comm, st));
     LEDGER(c, DP_COMM_GRAM, nG);
@@ -815,7 +836,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
     LEDGER(c, DP_COMM_GRAM, nG);
   }
   // (b) whitening node: A = G + kappa I, LDL^H, A^{-1}, beta (Lemma 1), z = A^{-1} s / beta
-  if (!topo_t1 || k.rank == 0) RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  if (!topo_t3 && (!topo_t1 || k.rank == 0)) RET(dispatch<Solve>(k.U, k.K, c, a, st));
   if (topo_t1) {
     // master broadcasts z and beta
     NK(ncclGroupStart());
@@ -949,8 +970,10 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   if (k.C % k.world) return fail(DP_ERR_INVALID, "C=%d not divisible by world=%d", k.C, k.world);
   if (!(k.Es > 0.0) || !std::isfinite(k.Es)) return fail(DP_ERR_INVALID, "Es must be > 0");
   if (!(k.tau >= 0.0) || !std::isfinite(k.tau)) return fail(DP_ERR_INVALID, "tau must be >= 0");
-  if (k.pd_topology != DP_PD_ALLREDUCE && k.pd_topology != DP_PD_REDUCE_BCAST)
+  if (k.pd_topology != DP_PD_ALLREDUCE && k.pd_topology != DP_PD_REDUCE_BCAST && k.pd_topology != DP_PD_SCATTER_GATHER)
     return fail(DP_ERR_INVALID, "pd_topology %d", k.pd_topology);
+  if (k.pd_topology == DP_PD_SCATTER_GATHER && k.n_sc % k.world)
+    return fail(DP_ERR_INVALID, "DP_PD_SCATTER_GATHER needs n_sc=%d divisible by world=%d", k.n_sc, k.world);
   if (k.U != 4 && k.U != 8 && k.U != 16 && k.U != 32)
     return fail(DP_ERR_UNSUPPORTED, "U=%d: supported U are 4, 8, 16, 32", k.U);
   const int S = k.B / k.C;

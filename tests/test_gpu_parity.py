@@ -410,7 +410,7 @@ def test_force_comm_world1_paths(cfgid):
     xr_pd, *_ = reference(cfg, f, "pd", N0)
     xr_fd, *_ = reference(cfg, f, "fd", N0)
     x_fd_plain, *_ = run(cfg, f, "fd", N0)
-    for topo in ("allreduce", "reduce_bcast"):
+    for topo in ("allreduce", "reduce_bcast", "scatter_gather"):
         x, beta, rx, pw, nbad = run(cfg, f, "pd", N0, flags=L.DP_FLAG_FORCE_COMM, nccl_id=uid,
                                     pd_topology=topo, s_on_all_ranks=False)
         assert nbad == 0 and rel_l2(x, xr_pd) <= REL_TOL

@@ -37,7 +37,8 @@ def test_library_payload_forms():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode,topology", [("pd", "allreduce"), ("pd", "reduce_bcast"), ("fd", "allreduce")])
+@pytest.mark.parametrize("mode,topology", [("pd", "allreduce"), ("pd", "reduce_bcast"), ("pd", "scatter_gather"),
+                                           ("fd", "allreduce")])
 def test_library_counters_match(mode, topology):
     import torch
 

@@ -5,7 +5,8 @@ pattern the library implements over NCCL:
 * NCCL-id bootstrap over torch.distributed;
 * max-over-ranks timing;
 * the distributed decomposition itself, evaluated with the oracle's steps:
-  PD  = local Gram -> allreduce (or reduce + z broadcast) -> solve -> local precode,
+  PD  = local Gram -> allreduce (or reduce + z broadcast, or reduce-scatter over subcarrier
+        blocks + z all-gather) -> solve -> local precode,
   FD  = s broadcast -> local clusters -> allreduce of [sum_c 1/beta_c, power],
   each equal to the single-process oracle.
 """
@@ -104,22 +105,33 @@ def w_pd_decomposition(rank, world):
     sh = D.cluster_shard(32, C, world, rank)
     Hl = f.H[:, sh.b0:sh.b1].astype(np.complex128)
     outs = {}
-    for topo in ("allreduce", "reduce_bcast"):
+    for topo in ("allreduce", "reduce_bcast", "scatter_gather"):
         # (a) local Gram: this rank's clusters (first adder-tree levels)
         G = torch.from_numpy(np.stack([oracle.gram(Hl[w]) for w in range(Hl.shape[0])]))
+        n_sc = Hl.shape[0]
+        nb = n_sc // world
+        mine = range(n_sc)                           # subcarriers this rank whitens
         if topo == "allreduce":
             dist.all_reduce(G)                       # every rank holds G
-        else:
+        elif topo == "reduce_bcast":
             dist.reduce(G, dst=0)                    # master holds G
-        z = torch.zeros((Hl.shape[0], 3, U), dtype=torch.complex128)
-        if topo == "allreduce" or rank == 0:
-            kappa = U * N0 / rho2
-            for w in range(Hl.shape[0]):
-                Ai = oracle.hpd_inverse(G[w].numpy() + kappa * np.eye(U))
-                beta = oracle.beta_lemma1(Ai, kappa, 1.0, rho2)
-                z[w] = torch.from_numpy((Ai @ f.s[w].T.astype(np.complex128)).T / beta)
+            mine = range(n_sc) if rank == 0 else range(0)
+        else:
+            # reduce-scatter over subcarrier blocks (gloo: all-reduce, keep this rank's block)
+            dist.all_reduce(G)
+            mine = range(rank * nb, (rank + 1) * nb)
+        z = torch.zeros((n_sc, 3, U), dtype=torch.complex128)
+        kappa = U * N0 / rho2
+        for w in mine:
+            Ai = oracle.hpd_inverse(G[w].numpy() + kappa * np.eye(U))
+            beta = oracle.beta_lemma1(Ai, kappa, 1.0, rho2)
+            z[w] = torch.from_numpy((Ai @ f.s[w].T.astype(np.complex128)).T / beta)
         if topo == "reduce_bcast":
             dist.broadcast(z, src=0)                 # master broadcasts z
+        elif topo == "scatter_gather":
+            blocks = [torch.zeros((nb, 3, U), dtype=torch.complex128) for _ in range(world)]
+            dist.all_gather(blocks, z[rank * nb:(rank + 1) * nb].contiguous())
+            z = torch.cat(blocks, dim=0)
         # (c) local precode x_c = H_c^H z
         x_local = np.einsum("wbu,wku->wkb", np.conj(Hl), z.numpy())
         x = D.gather_antennas(torch.from_numpy(x_local)).numpy()
@@ -165,7 +177,7 @@ def test_nccl_id_bootstrap_world2():
 
 def test_pd_exchange_pattern_world2():
     for r, errs in run_world("w_pd_decomposition").items():
-        assert errs["allreduce"] < 1e-12 and errs["reduce_bcast"] < 1e-12, errs
+        assert errs["allreduce"] < 1e-12 and errs["reduce_bcast"] < 1e-12 and errs["scatter_gather"] < 1e-12, errs
 
 
 def test_fd_exchange_pattern_world2():
