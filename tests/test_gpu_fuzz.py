@@ -1,0 +1,53 @@
+"""Randomised GPU parity sweep over the supported shape space (U, C, cluster size incl. B_c < U,
+K, n_sc incl. 1 and ragged, SNR), PD and FD against the fp64 oracle.  Seeded: the same cases every
+run.  Square clusters (B_c = U) are kept at <= 15 dB, where fp32 conditioning leaves margin to the
+1e-4 bar."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1804_10987_b200 import synth
+from paper_1804_10987_b200.api import Precoder
+
+from helpers import REL_TOL, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(seed: int):
+    rng = np.random.default_rng(1000 + seed)
+    U = int(rng.choice([4, 8, 16, 32]))
+    C = int(rng.choice([1, 2, 4, 8]))
+    sizes = [U, 2 * U, 4 * U] + [b for b in (4, 8, 16) if b < U]
+    S = int(rng.choice(sizes))
+    if S * C > 256:
+        C = max(1, 256 // S)
+    K = int(rng.integers(1, 21))
+    n_sc = int(rng.choice([1, 3, int(rng.integers(4, 41))]))
+    snr = float(rng.uniform(0.0, 15.0 if S <= U else 25.0))
+    M = int(rng.choice([4, 16, 64]))
+    return U, C, S, K, n_sc, snr, M
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_shapes(seed):
+    U, C, S, K, n_sc, snr, M = _case(seed)
+    B = S * C
+    f = synth.make_frame(50 + seed, n_sc, B, U, K, M)
+    N0 = synth.n0_from_snr_db(snr)
+    H = torch.from_numpy(f.H).cuda()
+    s = torch.from_numpy(f.s).cuda()
+    with Precoder(n_sc, B, U, K, C) as pre:
+        x_pd = pre.precode_pd(H, s, N0, 1.0).cpu().numpy()
+        x_fd = pre.precode_fd(H, s, N0, 1.0).cpu().numpy()
+        rx_fd = pre.read_scalars("rx").cpu().numpy()
+        assert pre.status() == 0
+    xr_pd, _ = oracle.pd(f.H, f.s, C, N0)
+    xr_fd, br = oracle.fd(f.H, f.s, C, N0, tau=0.125)
+    case = dict(U=U, C=C, S=S, K=K, n_sc=n_sc, snr=round(snr, 1), M=M)
+    assert rel_l2(x_pd, xr_pd) <= REL_TOL, (case, rel_l2(x_pd, xr_pd))
+    assert rel_l2(x_fd, xr_fd) <= REL_TOL, (case, rel_l2(x_fd, xr_fd))
+    assert np.max(np.abs(rx_fd / oracle.rx_scale_fd(br) - 1)) <= REL_TOL, case
