@@ -326,14 +326,15 @@ int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
   return DP_OK;
 }
 
-int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw);
+int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw,
+                int U = 32);
 
-template <int CH>
+template <int CH, int U>
 int launch_gram_tc2(dp_ctx *c, const Args &b, cudaStream_t st) {
-  using T = dpk::GT2<CH>;
+  using T = dpk::GT2<CH, U>;
   CUtensorMap tm;
-  RET(make_h_tmap(c, b.H, b.n_sc * b.Bl, &tm, CH, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
-  auto kern = dpk::gram_tc2_kernel<CH>;
+  RET(make_h_tmap(c, b.H, b.n_sc * b.Bl, &tm, CH, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, U));
+  auto kern = dpk::gram_tc2_kernel<CH, U>;
   CK(set_smem(kern, T::SMEM));
   LaunchScope ls(c, DP_KERNEL_GRAM, st);
   CK(launch_pdl(kern, dim3(std::min(b.n_sc * b.nchunks, c->num_sms)), dim3(T::THREADS), T::SMEM, st, tm, b));
@@ -342,15 +343,18 @@ int launch_gram_tc2(dp_ctx *c, const Args &b, cudaStream_t st) {
 
 template <int U, bool PER_CHUNK>
 int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
-  if constexpr (U == 32) {
-    if (c->use_tc && a.S % 32 == 0) {             // tensor-core Gram, operands straight from TMA
-      Args b = a;                                 // work item = (subcarrier, group)
-      if (!PER_CHUNK) {
-        b.S = a.Bl;                               // one group: all local antennas
-        b.nchunks = 1;
-      }
-      return (b.S % 64 == 0) ? launch_gram_tc2<64>(c, b, st) : launch_gram_tc2<32>(c, b, st);
+  if constexpr (U == 32 || U == 16) {
+    Args b = a;                                   // work item = (subcarrier, group)
+    if (!PER_CHUNK) {
+      b.S = a.Bl;                                 // one group: all local antennas
+      b.nchunks = 1;
     }
+    // tensor-core Gram, operands straight from TMA.  U = 16 (M = 64 UMMAs) is correct but measured
+    // no faster than the SIMT kernel at cfg3 (17.3 vs 15.5 us: 128-antenna items are too small to
+    // amortise the per-item epilogue), so it is opt-in (DP_GRAM_TC16)
+    static const bool tc16 = getenv("DP_GRAM_TC16") != nullptr;
+    if (c->use_tc && b.S % 32 == 0 && (U == 32 || tc16))
+      return (b.S % 64 == 0) ? launch_gram_tc2<64, U>(c, b, st) : launch_gram_tc2<32, U>(c, b, st);
   }
   const size_t sm = smem_gram(U, a.Bl, nw);
   if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "Gram tile needs %zu B of shared memory", sm);
@@ -402,7 +406,7 @@ int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
 
 // 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), box_rows-row x
 // 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
-int encode_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw) {
+int encode_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw, int U) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -410,8 +414,8 @@ int encode_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUte
         !encode)
       return fail(DP_ERR_CUDA, "cuTensorMapEncodeTiled not available");
   }
-  cuuint64_t dims[2] = {64, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {64 * 4};
+  cuuint64_t dims[2] = {(cuuint64_t)(2 * U), (cuuint64_t)rows};   // fp32 [rows][2U]
+  cuuint64_t strides[1] = {(cuuint64_t)(2 * U * 4)};
   cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)H, dims, strides, box, estr,
@@ -421,15 +425,16 @@ int encode_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUte
   return DP_OK;
 }
 
-int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw) {
+int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw, int U) {
+  const int key = (int)sw + 16 * U;
   for (const auto &e : c->tmaps)
-    if (e.p == H && e.rows == rows && e.box == box_rows && e.sw == (int)sw) {
+    if (e.p == H && e.rows == rows && e.box == box_rows && e.sw == key) {
       *tm = e.tm;
       return DP_OK;
     }
-  RET(encode_h_tmap(H, rows, tm, box_rows, sw));
+  RET(encode_h_tmap(H, rows, tm, box_rows, sw, U));
   if (c->tmaps.size() >= 16) c->tmaps.erase(c->tmaps.begin());
-  c->tmaps.push_back({H, rows, box_rows, (int)sw, *tm});
+  c->tmaps.push_back({H, rows, box_rows, key, *tm});
   return DP_OK;
 }
 

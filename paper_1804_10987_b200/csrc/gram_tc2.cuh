@@ -28,20 +28,24 @@
 
 namespace dpk {
 
-template <int CH> struct GT2 {
+// U = 32: 2 atoms of 32 reals per antenna row, M = 128, N = 64 (D rows = TMEM lanes);
+// U = 16: 1 atom, M = 64, N = 32 (an M = 64 accumulator: D row r in lane 32 (r / 16) + r % 16).
+template <int CH, int U> struct GT2 {
+  static constexpr int NA = U / 16;                        // 32-real atoms per antenna row
   static constexpr int BOX = CH * 128;                     // one TMA box: CH rows x 32 fp32
-  static constexpr int STAGE = 4 * BOX;                    // Xb (2 atoms) + Xs (2 atoms)
-  static constexpr int NS = CH == 64 ? 5 : 8;              // ring stages (160 / 128 KB)
-  static constexpr int LD = 68;                            // staging row stride (floats)
+  static constexpr int STAGE = 2 * NA * BOX;               // Xb (NA atoms) + Xs (NA atoms)
+  static constexpr int NS = (U == 32 ? (CH == 64 ? 5 : 8) : (CH == 64 ? 10 : 16));   // 160 / 128 KB
+  static constexpr int M = 4 * U, N = 2 * U;               // UMMA shape: A = [Xb^T; Xs^T], B = Xb^T
+  static constexpr int LD = N + 4;                         // staging row stride (floats)
   static constexpr int THREADS = 320;
-  static constexpr size_t SMEM = (size_t)NS * STAGE + 128 * LD * 4 + 1024;
+  static constexpr size_t SMEM = (size_t)NS * STAGE + M * LD * 4 + 1024;
 };
 
-template <int CH>
-__global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
+template <int CH, int U>
+__global__ void __launch_bounds__(GT2<CH, U>::THREADS, 1) gram_tc2_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
   pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
                    // (it still waits for this grid's completion in griddepcontrol.wait)
-  using T = GT2<CH>;
+  using T = GT2<CH, U>;
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
   float *stg = reinterpret_cast<float *>(sm + (size_t)T::NS * T::STAGE);
@@ -81,9 +85,9 @@ __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __g
           if (g >= T::NS) tc::mbar_wait(&stage_free[s], ph ^ 1);
           uint8_t *st = sm + (size_t)s * T::STAGE;
           const int row0 = item * a.S + c * CH;
-          tc::mbar_arrive_expect_tx(&full[s], 2 * T::BOX);
-          tc::tma_load_2d(st, &tmH, 0, row0, &full[s]);
-          tc::tma_load_2d(st + T::BOX, &tmH, 32, row0, &full[s]);
+          tc::mbar_arrive_expect_tx(&full[s], T::NA * T::BOX);
+#pragma unroll
+          for (int at = 0; at < T::NA; ++at) tc::tma_load_2d(st + at * T::BOX, &tmH, 32 * at, row0, &full[s]);
           if (++s == T::NS) { s = 0; ph ^= 1; }
         }
       }
@@ -91,12 +95,12 @@ __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __g
   } else if (warp == 9) {
     // ------------------------------------------------------------ UMMA issuer
     if (lane == 0) {
-      constexpr uint32_t IDESC = tc::idesc_tf32(128, 64) | (1u << 15) | (1u << 16);   // A, B MN-major
+      constexpr uint32_t IDESC = tc::idesc_tf32(T::M, T::N) | (1u << 15) | (1u << 16);   // A, B MN-major
       int s = 0, ph = 0, g = 0, n = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
         const int b = n & 1;
         if (n >= 2) tc::mbar_wait(&acc_empty[b], ((n >> 1) - 1) & 1);
-        const uint32_t d = tm + 64 * b;
+        const uint32_t d = tm + T::N * b;
         for (int c = 0; c < nck; ++c, ++g) {
           tc::mbar_wait(&prep_done[s], ph);
           tc::fence_after_sync();
@@ -121,8 +125,8 @@ __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __g
         tc::mbar_wait(&full[s], ph);
         uint8_t *st = sm + (size_t)s * T::STAGE;
         const uint4 *src = reinterpret_cast<const uint4 *>(st);
-        uint4 *dst = reinterpret_cast<uint4 *>(st + 2 * T::BOX);
-        constexpr int NV = 2 * T::BOX / 16 / 128;
+        uint4 *dst = reinterpret_cast<uint4 *>(st + T::NA * T::BOX);
+        constexpr int NV = T::NA * T::BOX / 16 / 128;
         uint4 v[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = src[ptid + 128 * i];
@@ -142,37 +146,42 @@ __global__ void __launch_bounds__(GT2<CH>::THREADS, 1) gram_tc2_kernel(const __g
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 0-3)
-    // TMEM lane r = D row r: r < 64 -> (Xb^T Xb)[r], r >= 64 -> (Xs^T Xb)[r - 64]
+    // D row r: r < 2U -> (Xb^T Xb)[r], r >= 2U -> (Xs^T Xb)[r - 2U]; TMEM lane of row r:
+    // r (M = 128) or 32 (r / 16) + r % 16 (M = 64: lanes 16..31 of each quarter unused)
     pdl_wait();                                       // Gout may still be read by the predecessor
+    constexpr int N = T::N;
+    const int myrow = (T::M == 128) ? tid : (lane < 16 ? 16 * warp + lane : -1);
     int n = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
       const int b = n & 1;
       tc::mbar_wait(&acc_full[b], (n >> 1) & 1);
       tc::fence_after_sync();
-      float d[64];
-      const uint32_t ta = tm + 64 * b + ((uint32_t)(32 * warp) << 16);
+      float d[N];
+      const uint32_t ta = tm + N * b + ((uint32_t)(32 * warp) << 16);
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb) tc::tmem_ld16_nowait(ta + 16 * cb, *reinterpret_cast<float(*)[16]>(d + 16 * cb));
+      for (int cb = 0; cb < N / 16; ++cb) tc::tmem_ld16_nowait(ta + 16 * cb, *reinterpret_cast<float(*)[16]>(d + 16 * cb));
       tc::tmem_wait_ld();
       tc::fence_before_sync();
       mbar_arrive(&acc_empty[b]);                     // accumulator free for item n + 2
       named_sync(1, 128);                             // previous item done with the staging
-      float4 *row = reinterpret_cast<float4 *>(stg + tid * T::LD);
+      if (myrow >= 0) {
+        float4 *row = reinterpret_cast<float4 *>(stg + myrow * T::LD);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) row[j] = make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
+        for (int j = 0; j < N / 4; ++j) row[j] = make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
+      }
       named_sync(1, 128);
-      // P = D1 + D2 + D2^T ; D1 = stg rows 0..63, D2 = stg rows 64..127
+      // P = D1 + D2 + D2^T ; D1 = stg rows 0..N-1, D2 = stg rows N..2N-1
       auto P = [&](int r, int q) {
-        return stg[r * T::LD + q] + stg[(64 + r) * T::LD + q] + stg[(64 + q) * T::LD + r];
+        return stg[r * T::LD + q] + stg[(N + r) * T::LD + q] + stg[(N + q) * T::LD + r];
       };
-      float2 *out = a.Gout + (size_t)item * npacked(32);
+      float2 *out = a.Gout + (size_t)item * npacked(U);
 #pragma unroll 2
-      for (int e = tid; e < 32 * 32; e += 128) {
-        const int u = e >> 5, v = e & 31;
+      for (int e = tid; e < U * U; e += 128) {
+        const int u = e / U, v = e % U;
         if (u <= v) {
           const float gr = P(2 * u, 2 * v) + P(2 * u + 1, 2 * v + 1);
           const float gi = P(2 * u + 1, 2 * v) - P(2 * u, 2 * v + 1);
-          out[pidx(32, u, v)] = make_float2(gr, gi);
+          out[pidx(U, u, v)] = make_float2(gr, gi);
         }
       }
     }
