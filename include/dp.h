@@ -234,6 +234,11 @@ DP_API int dp_debug_solve(dp_ctx *ctx, const dp_c32 *G_packed, int groups, const
 DP_API int dp_prepare_pd(dp_ctx *ctx, const dp_c32 *H_local, double N0, double rho2, void *stream);
 DP_API int dp_prepare_fd(dp_ctx *ctx, const dp_c32 *H_local, double N0, double rho2, void *stream);
 DP_API int dp_apply(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s, int Ka, dp_c32 *x_local, void *stream);
+/* Prepare from a Gram the caller already holds (uplink/downlink reuse of H_c H_c^H):
+ * fd = 0: G_packed [n_sc][U(U+1)/2] = this rank's sum over its clusters (summed across ranks here);
+ * fd = 1: G_packed [n_sc][C/world][U(U+1)/2] per local cluster; packed upper triangle, row-major
+ * (u <= v), the layout of dp_debug_gram.  Then dp_apply as after dp_prepare_pd / dp_prepare_fd. */
+DP_API int dp_prepare_from_gram(dp_ctx *ctx, int fd, const dp_c32 *G_packed, double N0, double rho2, void *stream);
 
 /* --------------------------------------------------------------------------
  * Uncoded-BER harness (Sec. IV-D "Simulation Results", P:236-242,

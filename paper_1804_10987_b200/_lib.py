@@ -26,7 +26,7 @@ EXPORTS = [
     "dp_get_unique_id", "dp_init", "dp_precode_pd", "dp_precode_fd", "dp_read_scalars",
     "dp_status", "dp_profile_read", "dp_launch_count", "dp_finalize", "dp_last_error",
     "dp_debug_gram", "dp_debug_solve", "dp_synth_frame", "dp_receive_count",
-    "dp_prepare_pd", "dp_prepare_fd", "dp_apply", "dp_comm_ledger", "dp_precode_mrt",
+    "dp_prepare_pd", "dp_prepare_fd", "dp_apply", "dp_comm_ledger", "dp_precode_mrt", "dp_prepare_from_gram",
 ]
 
 
@@ -74,6 +74,7 @@ def lib() -> ctypes.CDLL:
     L.dp_prepare_pd.argtypes = [P, P, D, D, P]
     L.dp_prepare_fd.argtypes = [P, P, D, D, P]
     L.dp_apply.argtypes = [P, P, P, I, P, P]
+    L.dp_prepare_from_gram.argtypes = [P, I, P, D, D, P]
     U64 = ctypes.c_ulonglong
     L.dp_synth_frame.argtypes = [U64, U64, I, I, I, I, I, D, P, P, P, P, P]
     L.dp_receive_count.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P]
@@ -178,3 +179,7 @@ def dp_comm_ledger(ctx, reset: bool = False) -> dict:
     out = (ctypes.c_longlong * DP_NUM_COMM)()
     check(lib().dp_comm_ledger(ctx, out, int(reset)), "dp_comm_ledger")
     return {k: int(out[i]) for i, k in enumerate(COMM_KINDS)}
+
+
+def dp_prepare_from_gram(ctx, fd: bool, G_ptr: int, N0: float, rho2: float, stream: int) -> int:
+    return lib().dp_prepare_from_gram(ctx, int(fd), G_ptr, float(N0), float(rho2), stream)

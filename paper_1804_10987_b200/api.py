@@ -105,6 +105,14 @@ class Precoder:
         L.check(L.dp_prepare_fd(self.ctx, _ptr(H), N0, rho2, self._stream(stream)), "dp_prepare_fd")
         self._prepared = "dp_precode_fd"
 
+    def prepare_from_gram(self, G, mode: str, N0: float, rho2: float = 1.0, stream=None):
+        """Prepare from a Gram already computed (uplink reuse): G [n_sc][U(U+1)/2] (PD) or
+        [n_sc][C/world][U(U+1)/2] (FD), packed upper triangle (the layout debug_gram returns)."""
+        fd = mode == "fd"
+        L.check(L.dp_prepare_from_gram(self.ctx, fd, _ptr(G.contiguous()), N0, rho2, self._stream(stream)),
+                "dp_prepare_from_gram")
+        self._prepared = "dp_precode_fd" if fd else "dp_precode_pd"
+
     def apply(self, H, s, out=None, stream=None):
         """x_local = H_local^H W s for s [n_sc][Ka][U], 1 <= Ka <= K (the prepared mode's W)."""
         Ka = s.shape[1] if s is not None else self.K

@@ -1196,6 +1196,37 @@ int dp_debug_solve(dp_ctx *c, const dp_c32 *G, int groups, const dp_c32 *s, doub
 }
 
 // ---------------------------------------------------------------- prepare / apply (f2)
+// Prepare from a Gram the caller already has (uplink reuse): G_packed holds this rank's
+// partial Gram(s) in the packed layout of dp_debug_gram; it is copied into the context and the
+// prepare continues as from the Gram kernel's output.
+int prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G, double N0, double rho2, cudaStream_t st) {
+  const dp_config &k = c->cfg;
+  const int groups = fd ? c->Cl : 1;
+  const size_t nG = (size_t)k.n_sc * groups * dpk::npacked(k.U);
+  CK(cudaMemcpyAsync(c->G, G, nG * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+  Args a = base_args(c);
+  if (fd) {
+    const double rho_c2 = rho2 / k.C;
+    a.kappa = (float)(k.tau * k.U * N0 / rho_c2);          // Eq. 9
+    a.coef = (float)(k.Es / rho_c2);
+  } else {
+    a.kappa = (float)(k.U * N0 / rho2);                    // Eq. 5
+    a.coef = (float)(k.Es / rho2);
+    if (c->comm_on) {
+      NK(ncclAllReduce(c->G, c->G, nG * 2, ncclFloat, ncclSum, c->comm, st));
+      LEDGER(c, DP_COMM_GRAM, nG * 2);
+    }
+  }
+  a.groups = groups;
+  a.nbeta = groups;
+  a.G = c->G;
+  a.Wout = c->G;
+  a.s = nullptr;
+  RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  c->prepared = fd;
+  return DP_OK;
+}
+
 int dp_prepare_pd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stream) {
   g_err.clear();
   if (!c || !H) return fail(DP_ERR_INVALID, "ctx and H_local must be non-NULL");
@@ -1254,6 +1285,18 @@ int dp_prepare_fd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
   RET(dispatch<Solve>(k.U, k.K, c, a, st));
   c->prepared = 1;
   return DP_OK;
+}
+
+int dp_prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G_packed, double N0, double rho2, void *stream) {
+  g_err.clear();
+  if (!c || !G_packed) return fail(DP_ERR_INVALID, "ctx and G_packed must be non-NULL");
+  if (!is_device_ptr(c, G_packed)) return fail(DP_ERR_INVALID, "dp_prepare_from_gram takes device pointers");
+  if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
+  if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");
+  if (fd != 0 && fd != 1) return fail(DP_ERR_INVALID, "fd must be 0 (PD) or 1 (FD)");
+  if (fd && c->S < c->cfg.U) return fail(DP_ERR_UNSUPPORTED, "prepare/apply: FD branch B_c < U runs fused only");
+  CK(cudaSetDevice(c->cfg.device));
+  return prepare_from_gram(c, fd, G_packed, N0, rho2, (cudaStream_t)stream);
 }
 
 int dp_apply(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, int Ka, dp_c32 *x, void *stream) {

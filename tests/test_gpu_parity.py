@@ -353,6 +353,28 @@ def test_prepare_apply_matches_oracle(cfgid, mode):
         assert pre.status() == 0
 
 
+@pytest.mark.parametrize("mode", ["pd", "fd"])
+def test_prepare_from_uplink_gram(mode):
+    """Uplink Gram reuse: a Gram supplied by the caller (here the fp64 oracle's, rounded to
+    complex64) instead of the Gram kernel; apply gives the frame's x."""
+    cfg = CONFIGS[3]
+    f = frame(cfg, 19)
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    xr, *_ = reference(cfg, f, mode, N0)
+    S, U = cfg.S, cfg.U
+    iu = np.triu_indices(U)
+    if mode == "pd":
+        G = np.stack([oracle.gram(f.H[w])[iu] for w in range(19)])
+    else:
+        G = np.stack([[oracle.gram(f.H[w, c * S:(c + 1) * S])[iu] for c in range(cfg.C)] for w in range(19)])
+    Gt = torch.from_numpy(G.astype(np.complex64)).cuda()
+    with Precoder(19, cfg.B, U, cfg.K, cfg.C, tau=cfg.tau) as pre:
+        pre.prepare_from_gram(Gt, mode, N0, 1.0)
+        x = pre.apply(torch.from_numpy(f.H).cuda(), torch.from_numpy(f.s).cuda())
+        assert pre.status() == 0
+    assert rel_l2(x.cpu().numpy(), xr) <= REL_TOL
+
+
 def test_apply_without_prepare_rejected():
     cfg = CONFIGS[2]
     f = frame(cfg, 5)
