@@ -101,7 +101,9 @@ typedef struct {
     int B;               /* BS antennas (all ranks), > 0                                        */
     int U;               /* UEs, 1 <= U <= 32                                                   */
     int K;               /* OFDM symbols per frame sharing one channel, 1..64           */
-    int C;               /* antenna clusters, B % C == 0, C % world == 0, B/C >= U              */
+    int C;               /* antenna clusters, C % world == 0, B % world == 0.  B % C == 0 gives the
+                            equal split B_c = B/C (B/C >= U or in {4, 8, 16}); otherwise FD / MRT
+                            need dp_set_clusters first (unequal B_c)                     */
     int rank, world;     /* this process's rank and the number of GPUs (one process per GPU)    */
     int device;          /* CUDA device ordinal of this rank                                    */
     const void *nccl_id; /* 128-byte ncclUniqueId from dp_get_unique_id on rank 0, identical on
@@ -162,9 +164,22 @@ DP_API int dp_precode_pd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
 DP_API int dp_precode_fd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
                   double N0, double rho2, dp_c32 *x_local, void *stream);
 
-/* Copy scalar output `which` (DP_SCALAR_*) of the last precode call into
- * `dst` (device or host float array of the documented length), ordered on
- * `stream`; a host `dst` is complete when the call returns. */
+/* Unequal clusters, per-cluster power and tau ("B_c = w_c B", P:215 with its footnote,
+ * Eq. 9 "tau_c").  Host arrays over ALL C clusters (global order), copied:
+ *   B_c[C]    cluster sizes, sum = B; each rank's clusters (c in [rank C/world, (rank+1) C/world))
+ *             must hold B/world antennas; B_c < U needs B_c in {4, 8, 16} (small-cluster branch);
+ *             NULL = the equal split B/C;
+ *   power[C]  shares w_c = rho_c^2 / rho2 > 0 with sum_c w_c = 1 (within 1e-9); NULL = 1/C each;
+ *   tau[C]    tau_c >= 0; NULL = cfg.tau for every cluster.
+ * Applies to dp_precode_fd and dp_precode_mrt (kappa_c = tau_c U N0 / rho_c^2, beta_c^2 =
+ * Es tr(Q_c^H Q_c) / rho_c^2); PD does not depend on the partition.  The equal split with
+ * equal shares and cfg.tau restores the default path.  DP_FLAG_UNFUSED, dp_prepare_fd and
+ * dp_apply after dp_prepare_fd return DP_ERR_UNSUPPORTED while clusters are unequal.
+ * Cluster c of a rank starts at local antenna row sum_{c' < c, same rank} B_c'.  The rank's
+ * clusters run as maximal runs of equal (B_c, w_c, tau_c), one launch each (at most 64 runs).
+ * Errors: DP_ERR_INVALID (sums, signs, NULL ctx), DP_ERR_UNSUPPORTED (sizes the kernels lack). */
+DP_API int dp_set_clusters(dp_ctx *ctx, const int *B_c, const double *power, const double *tau);
+
 /* Fully-distributed MRT (the baseline of Fig. 2): per cluster the
  * matched filter x_c = H_c^H s / beta_c with beta_c = sqrt(Es ||H_c||_F^2 / rho_c^2),
  * rho_c^2 = rho2 / C (Eq. 5 applied to the cluster).  N0 is accepted and ignored.
@@ -174,6 +189,9 @@ DP_API int dp_precode_fd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
 DP_API int dp_precode_mrt(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
                   double N0, double rho2, dp_c32 *x_local, void *stream);
 
+/* Copy scalar output `which` (DP_SCALAR_*) of the last precode call into
+ * `dst` (device or host float array of the documented length), ordered on
+ * `stream`; a host `dst` is complete when the call returns. */
 DP_API int dp_read_scalars(dp_ctx *ctx, int which, float *dst, void *stream);
 
 /* Synchronize the context's work and report the number of (subcarrier,

@@ -56,6 +56,8 @@ def _L():
         lib.oracle_fd.argtypes = [P, I, I, I, I, I, P, D, D, D, D, P, P]
         lib.oracle_rx_scale_fd.argtypes = [P, I, I, P]
         lib.oracle_mrt_fd.argtypes = [P, I, I, I, I, I, P, D, D, P, P]
+        lib.oracle_fd_var.argtypes = [P, I, I, I, I, I, P, P, P, P, D, D, P, P]
+        lib.oracle_mrt_fd_var.argtypes = [P, I, I, I, I, I, P, P, P, D, P, P]
         lib.oracle_num_threads.restype = I
         _lib = lib
     return _lib
@@ -179,6 +181,45 @@ def mrt_fd(H, s, C: int, rho2: float = 1.0, Es: float = 1.0):
     x = np.empty((n_sc, K, B), np.complex128)
     beta_c = np.empty((n_sc, C), np.float64)
     _check(_L().oracle_mrt_fd(_p(H), n_sc, B, U, K, C, _p(s), rho2, Es, _p(x), _p(beta_c)), "mrt_fd")
+    return x, beta_c
+
+
+def _var_args(sizes, power, tau, C, rho2):
+    B_c = np.ascontiguousarray(sizes, dtype=np.int32)
+    w = np.full(C, 1.0 / C) if power is None else np.asarray(power, dtype=np.float64)
+    rho2_c = np.ascontiguousarray(w * rho2, dtype=np.float64)
+    t = np.ascontiguousarray(np.broadcast_to(np.asarray(tau, dtype=np.float64), (C,)))
+    return B_c, rho2_c, t
+
+
+def fd_var(H, s, sizes, N0: float, rho2: float = 1.0, Es: float = 1.0, power=None, tau=0.125,
+           allow_numeric=False):
+    """FD-WF with unequal clusters B_c (P:157), power shares rho_c^2 = power_c rho^2 (P:213-215;
+    default 1/C) and per-cluster tau_c (Eq. 9; scalar or sequence).  Returns (x, beta_c[n_sc][C])."""
+    H, s = _c128(H), _c128(s)
+    n_sc, B, U = H.shape
+    K = s.shape[1]
+    C = len(sizes)
+    B_c, rho2_c, t = _var_args(sizes, power, tau, C, rho2)
+    x = np.empty((n_sc, K, B), np.complex128)
+    beta_c = np.empty((n_sc, C), np.float64)
+    rc = _L().oracle_fd_var(_p(H), n_sc, B, U, K, C, _p(B_c), _p(rho2_c), _p(t), _p(s), N0, Es, _p(x),
+                            _p(beta_c))
+    _check(rc, "fd_var", allow_numeric)
+    return x, beta_c
+
+
+def mrt_fd_var(H, s, sizes, rho2: float = 1.0, Es: float = 1.0, power=None):
+    """Fully-distributed MRT with unequal clusters and power shares.  Returns (x, beta_c[n_sc][C])."""
+    H, s = _c128(H), _c128(s)
+    n_sc, B, U = H.shape
+    K = s.shape[1]
+    C = len(sizes)
+    B_c, rho2_c, _ = _var_args(sizes, power, 0.0, C, rho2)
+    x = np.empty((n_sc, K, B), np.complex128)
+    beta_c = np.empty((n_sc, C), np.float64)
+    _check(_L().oracle_mrt_fd_var(_p(H), n_sc, B, U, K, C, _p(B_c), _p(rho2_c), _p(s), Es, _p(x), _p(beta_c)),
+           "mrt_fd_var")
     return x, beta_c
 
 

@@ -405,6 +405,104 @@ int oracle_fd(const cplx *H, int n_sc, int B, int U, int K, int C, const cplx *s
 }
 
 /* ------------------------------------------------------------------------ */
+/* FD-WF with unequal clusters: the same per-cluster precoder  */
+/* as oracle_fd with the partition and the power split of the paper's        */
+/* general statement instead of the equal one:                               */
+/*   B_c = w_c B, sum_c B_c = B, cluster c = antennas sum_{c'<c} B_c' ...    */
+/*                                                                     */
+/*   rho_c^2 given, sum_c rho_c^2 = rho^2        */
+/*   kappa_c = tau_c U N0 / rho_c^2                        (Eq. 9)     */
+/*   Q_c by the branch of P:227-233 for each B_c; beta_c and x_c as in P:217. */
+/* rho2_c[C] and tau_c[C] are per cluster; beta_c out [n_sc][C].             */
+/* ------------------------------------------------------------------------ */
+int oracle_fd_var(const cplx *H, int n_sc, int B, int U, int K, int C, const int *B_c,
+                  const double *rho2_c, const double *tau_c, const cplx *s, double N0, double Es,
+                  cplx *x, double *beta_c)
+{
+    if (!H || !s || !x || !beta_c || !B_c || !rho2_c || !tau_c || n_sc <= 0 || B <= 0 || U <= 0 ||
+        K <= 0 || C <= 0 || N0 < 0 || !(Es > 0))
+        return ERR_ARG;
+    int tot = 0, Smax = 0;
+    for (int c = 0; c < C; ++c) {
+        if (B_c[c] <= 0 || !(rho2_c[c] > 0) || tau_c[c] < 0) return ERR_ARG;
+        tot += B_c[c];
+        if (B_c[c] > Smax) Smax = B_c[c];
+    }
+    if (tot != B) return ERR_ARG;
+    int rc = OK;
+#pragma omp parallel for schedule(dynamic) reduction(max : rc)
+    for (int w = 0; w < n_sc; ++w) {
+        const cplx *Hw = H + (size_t)w * B * U;
+        cplx *Q = malloc(sizeof(cplx) * Smax * U);
+        int off = 0;
+        for (int c = 0; c < C; ++c) {
+            const int S = B_c[c];
+            const cplx *Hc = Hw + (size_t)off * U;
+            const double kappa_c = tau_c[c] * U * N0 / rho2_c[c];
+            int r = fd_cluster_Q(Hc, S, U, kappa_c, Q);
+            double fro = 0.0;
+            for (int i = 0; i < S * U; ++i) fro += creal(Q[i] * conj(Q[i]));
+            double rr = fro * Es / rho2_c[c];
+            double bc = (r == OK && rr > 0.0 && isfinite(rr)) ? sqrt(rr) : NAN;
+            if (r == OK && !isfinite(bc)) r = ERR_NUMERIC;
+            beta_c[(size_t)w * C + c] = bc;
+            for (int k = 0; k < K; ++k) {
+                const cplx *sk = s + ((size_t)w * K + k) * U;
+                cplx *xk = x + ((size_t)w * K + k) * B + off;
+                for (int b = 0; b < S; ++b) {
+                    cplx acc = 0;
+                    for (int u = 0; u < U; ++u) acc += Q[(size_t)b * U + u] * sk[u];
+                    xk[b] = (r == OK) ? acc / bc : 0.0;
+                }
+            }
+            if (r > rc) rc = r;
+            off += S;
+        }
+        free(Q);
+    }
+    return rc;
+}
+
+/* Fully-distributed MRT with unequal clusters: Q_c = H_c^H, beta_c =        */
+/* sqrt(Es ||H_c||_F^2 / rho_c^2) per cluster of size B_c.    */
+int oracle_mrt_fd_var(const cplx *H, int n_sc, int B, int U, int K, int C, const int *B_c,
+                      const double *rho2_c, const cplx *s, double Es, cplx *x, double *beta_c)
+{
+    if (!H || !s || !x || !beta_c || !B_c || !rho2_c || n_sc <= 0 || B <= 0 || U <= 0 || K <= 0 ||
+        C <= 0 || !(Es > 0))
+        return ERR_ARG;
+    int tot = 0;
+    for (int c = 0; c < C; ++c) {
+        if (B_c[c] <= 0 || !(rho2_c[c] > 0)) return ERR_ARG;
+        tot += B_c[c];
+    }
+    if (tot != B) return ERR_ARG;
+    for (int w = 0; w < n_sc; ++w) {
+        const cplx *Hw = H + (size_t)w * B * U;
+        int off = 0;
+        for (int c = 0; c < C; ++c) {
+            const int S = B_c[c];
+            const cplx *Hc = Hw + (size_t)off * U;
+            double fro = 0.0;
+            for (int i = 0; i < S * U; ++i) fro += creal(Hc[i] * conj(Hc[i]));
+            const double bc = sqrt(Es * fro / rho2_c[c]);
+            beta_c[(size_t)w * C + c] = bc;
+            for (int k = 0; k < K; ++k) {
+                const cplx *sk = s + ((size_t)w * K + k) * U;
+                cplx *xk = x + ((size_t)w * K + k) * B + off;
+                for (int b = 0; b < S; ++b) {
+                    cplx acc = 0;
+                    for (int u = 0; u < U; ++u) acc += conj(Hc[(size_t)b * U + u]) * sk[u];
+                    xk[b] = bc > 0.0 ? acc / bc : 0.0;
+                }
+            }
+            off += S;
+        }
+    }
+    return OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Fully-distributed MRT, the baseline of Fig. 2: per   */
 /* cluster the matched filter Q_c = H_c^H with the per-cluster power split    */
 /* rho_c^2 = rho^2 / C and the normalisation of Eq. (5) applied to    */

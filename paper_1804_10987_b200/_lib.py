@@ -27,6 +27,7 @@ EXPORTS = [
     "dp_status", "dp_profile_read", "dp_launch_count", "dp_finalize", "dp_last_error",
     "dp_debug_gram", "dp_debug_solve", "dp_synth_frame", "dp_receive_count",
     "dp_prepare_pd", "dp_prepare_fd", "dp_apply", "dp_comm_ledger", "dp_precode_mrt", "dp_prepare_from_gram",
+    "dp_set_clusters",
 ]
 
 
@@ -75,6 +76,7 @@ def lib() -> ctypes.CDLL:
     L.dp_prepare_fd.argtypes = [P, P, D, D, P]
     L.dp_apply.argtypes = [P, P, P, I, P, P]
     L.dp_prepare_from_gram.argtypes = [P, I, P, D, D, P]
+    L.dp_set_clusters.argtypes = [P, P, P, P]
     U64 = ctypes.c_ulonglong
     L.dp_synth_frame.argtypes = [U64, U64, I, I, I, I, I, D, P, P, P, P, P]
     L.dp_receive_count.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P]
@@ -113,6 +115,13 @@ def dp_precode_fd(ctx, H_ptr: int, s_ptr: int, N0: float, rho2: float, x_ptr: in
 
 def dp_precode_mrt(ctx, H_ptr: int, s_ptr: int, N0: float, rho2: float, x_ptr: int, stream: int) -> int:
     return lib().dp_precode_mrt(ctx, H_ptr, s_ptr, float(N0), float(rho2), x_ptr, stream)
+
+
+def dp_set_clusters(ctx, B_c=None, power=None, tau=None) -> int:
+    """Sequences of C cluster sizes / power shares / tau values (None = the default)."""
+    def arr(ct, v):
+        return None if v is None else (ct * len(v))(*v)
+    return lib().dp_set_clusters(ctx, arr(ctypes.c_int, B_c), arr(ctypes.c_double, power), arr(ctypes.c_double, tau))
 
 
 def dp_read_scalars(ctx, which: int, dst_ptr: int, stream: int) -> int:

@@ -92,6 +92,14 @@ class Precoder:
         """FD-WF (Sec. III-C): per-cluster WF with rho_c^2 = rho^2/C, kappa_c = tau U N0/rho_c^2."""
         return self._run(L.dp_precode_fd, "dp_precode_fd", H, s, N0, rho2, out, stream)
 
+    def set_clusters(self, sizes=None, power=None, tau=None):
+        """Unequal clusters B_c = w_c B, power shares rho_c^2 / rho^2 (P:215 footnote) and
+        per-cluster tau_c (Eq. 9) for precode_fd / precode_mrt; sequences over all C clusters,
+        None = the default (equal split, 1/C, the constructor's tau).  include/dp.h dp_set_clusters."""
+        L.check(L.dp_set_clusters(self.ctx, None if sizes is None else [int(v) for v in sizes],
+                                  None if power is None else [float(v) for v in power],
+                                  None if tau is None else [float(v) for v in tau]), "dp_set_clusters")
+
     # ------------------------------------------------------------ prepare / apply (P:286-289)
     def prepare_pd(self, H, N0: float, rho2: float = 1.0, stream=None):
         """Cache W = A^{-1}/beta^WF for this channel (PD); then apply() per batch of symbols."""

@@ -102,6 +102,11 @@ struct dp_ctx {
   struct TmapEntry { const void *p; int rows, box, sw; CUtensorMap tm; };
   std::vector<TmapEntry> tmaps;
   std::vector<std::pair<const void *, bool>> ptr_kind;
+  // unequal clusters (dp_set_clusters; Eq. 9): this rank's clusters as maximal
+  // runs of equal (size, power share, tau); empty = the equal split B/C, rho^2/C, cfg.tau
+  struct VarRun { int cl0, len, S, off; double w, tau; };
+  std::vector<VarRun> vruns;
+  std::vector<int> vsizes;   // all C cluster sizes (global) when set
   // last call
   int last_mode = -1;        // 0 pd, 1 fd
   int prepared = -1;         // W cached in G by dp_prepare_pd (0) / dp_prepare_fd (1); -1 none
@@ -466,7 +471,7 @@ bool fd_tc_ok(const dp_ctx *c, const Args &a) {
 // CTAs) or a CTA holds whole subcarriers (Cl = 1, 2, 4).  Returns CTAs per subcarrier, 0 = off.
 int fd_fold_of(const dp_ctx *c, const Args &a) {
   static const bool off = getenv("DP_NO_FOLD") != nullptr;
-  if (off || a.Gout) return 0;
+  if (off || a.Gout || !c->vruns.empty()) return 0;
   const int Cl = a.nchunks;
   if (Cl == 4 || Cl == 8 || Cl == 16 || Cl == 32) return Cl / 4;
   if (4 % Cl == 0) return 1;
@@ -476,14 +481,15 @@ int fd_fold_of(const dp_ctx *c, const Args &a) {
 template <int KC, bool WTC>
 int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
-  RET(make_h_tmap(c, a.H, a.n_sc * a.Bl, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  RET(make_h_tmap(c, a.H, a.n_sc * a.Bl - a.hrow_off, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   auto kern = dpk::fd_tc_kernel<KC, WTC>;
   static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
   const size_t smem = dpk::FDT_SMEM + pad;
   CK(set_smem(kern, smem));
   const int nprob = a.n_sc * a.nchunks;
   Args b = a;
-  b.pf_dist = 3 * c->num_sms;                                // resident CTAs: 3 per SM
+  // resident CTAs: 3 per SM; the L2 prefetch assumes contiguous clusters (off for unequal runs)
+  b.pf_dist = a.Bl == a.nchunks * 32 ? 3 * c->num_sms : 0;
   b.fold = fd_fold_of(c, a);
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
   if (b.fold > 1)
@@ -684,9 +690,68 @@ int finish_call(dp_ctx *c, bool host, dp_c32 *x, cudaStream_t st) {
 }
 
 // FD frame on device pointers (everything after the host staging)
+// Unequal clusters (dp_set_clusters): one launch per run of equal (B_c, rho_c^2 share, tau_c)
+// -- the same kernels as the equal split, H / x offset to the run's first antenna with the
+// rank's row stride Bl -- into per-run beta / power scratch, then fd_var_finish_kernel
+// (beta_c in [sc][Cl] order, fin = {sum_c 1/beta_c, sum_c power_c}).  mrt: the MRT precoder.
+int launch_mrt_u(dp_ctx *c, const Args &a, cudaStream_t st);
+// FD / MRT need cluster sizes: the equal split, or dp_set_clusters when C does not divide B
+int need_split(const dp_ctx *c) {
+  if (c->S == 0 && c->vruns.empty())
+    return fail(DP_ERR_INVALID, "B=%d not divisible by C=%d: set the cluster sizes with dp_set_clusters", c->cfg.B,
+                c->cfg.C);
+  return DP_OK;
+}
+int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, double rho2, float2 *xd, bool mrt,
+                cudaStream_t st) {
+  const dp_config &k = c->cfg;
+  const size_t n = (size_t)k.n_sc * c->Cl;
+  float *vb = nullptr;
+  CK(cudaMallocAsync((void **)&vb, 2 * n * sizeof(float), st));
+  dpk::VarRuns vr;
+  memset(&vr, 0, sizeof(vr));
+  vr.n = (int)c->vruns.size();
+  vr.Cl = c->Cl;
+  vr.vb = vb;
+  vr.vp = vb + n;
+  int rc = DP_OK;
+  for (int i = 0; i < vr.n && rc == DP_OK; ++i) {
+    const auto &r = c->vruns[i];
+    const double rho_c2 = r.w * rho2;                     // rho_c^2 = w_c rho^2, sum_c w_c = 1
+    Args a = base_args(c);
+    a.H = Hd + (size_t)r.off * k.U;
+    a.hrow_off = r.off;
+    a.s = s_use;
+    a.x = xd + r.off;
+    a.S = r.S;
+    a.nchunks = r.len;
+    a.nbeta = r.len;
+    a.kappa = (float)(r.tau * k.U * N0 / rho_c2);         // Eq. 9 with the cluster's tau_c, rho_c^2
+    a.coef = (float)(k.Es / rho_c2);
+    a.beta = vb + (size_t)k.n_sc * r.cl0;
+    a.pw = vb + n + (size_t)k.n_sc * r.cl0;
+    a.fold = 0;
+    vr.cl0[i] = r.cl0;
+    vr.len[i] = r.len;
+    if (mrt) rc = launch_mrt_u(c, a, st);
+    else if (r.S < k.U) rc = launch_fd_small(c, a, st);
+    else if (fd_tc_ok(c, a)) rc = launch_fd_tc_kc(c, a, st);
+    else rc = dispatch<FdFused>(k.U, k.K, c, a, st);
+  }
+  if (rc == DP_OK) {
+    Args a = base_args(c);
+    LaunchScope ls(c, DP_KERNEL_FINISH, st);
+    const cudaError_t e = launch_pdl(dpk::fd_var_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a, vr);
+    if (e != cudaSuccess) rc = fail(DP_ERR_CUDA, "fd_var_finish_kernel: %s", cudaGetErrorString(e));
+  }
+  CK(cudaFreeAsync(vb, st));
+  return rc;
+}
+
 int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, double rho2, float2 *xd,
                    cudaStream_t st) {
   const dp_config &k = c->cfg;
+  RET(need_split(c));
   const float2 *s_use;
   RET(distribute_s(c, sd, st, &s_use));
   // FD parameters (Sec. III-C): rho_c^2 = rho^2/C, kappa_c = tau U N0 / rho_c^2 (Eq. 9)
@@ -700,7 +765,10 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   a.kappa = (float)(k.tau * k.U * N0 / rho_c2);
   a.coef = (float)(k.Es / rho_c2);
   a.nbeta = c->Cl;
-  if (c->S < k.U) {
+  if (!c->vruns.empty()) {
+    if (k.flags & DP_FLAG_UNFUSED) return fail(DP_ERR_UNSUPPORTED, "DP_FLAG_UNFUSED with unequal clusters");
+    RET(fd_var_runs(c, Hd, s_use, N0, rho2, xd, false, st));
+  } else if (c->S < k.U) {
     // small clusters (B_c < U): B_c x B_c regularised Gram per cluster
     RET(launch_fd_small(c, a, st));
     LaunchScope ls(c, DP_KERNEL_FINISH, st);
@@ -752,10 +820,19 @@ int launch_mrt(dp_ctx *c, const Args &a, cudaStream_t st) {
   CK(launch_pdl(kern, dim3((a.n_sc * a.nchunks + 3) / 4), dim3(128), sm, st, a));
   return DP_OK;
 }
+int launch_mrt_u(dp_ctx *c, const Args &a, cudaStream_t st) {
+  switch (c->cfg.U) {
+    case 4: return launch_mrt<4>(c, a, st);
+    case 8: return launch_mrt<8>(c, a, st);
+    case 16: return launch_mrt<16>(c, a, st);
+    default: return launch_mrt<32>(c, a, st);
+  }
+}
 int precode_mrt_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, double rho2, float2 *xd,
                     cudaStream_t st) {
   (void)N0;                                               // MRT ignores the noise level
   const dp_config &k = c->cfg;
+  RET(need_split(c));
   const float2 *s_use;
   RET(distribute_s(c, sd, st, &s_use));
   Args a = base_args(c);
@@ -766,13 +843,10 @@ int precode_mrt_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, do
   a.nchunks = c->Cl;
   a.coef = (float)(k.Es / (rho2 / k.C));                  // Es / rho_c^2, rho_c^2 = rho^2 / C
   a.nbeta = c->Cl;
-  switch (k.U) {
-    case 4: RET(launch_mrt<4>(c, a, st)); break;
-    case 8: RET(launch_mrt<8>(c, a, st)); break;
-    case 16: RET(launch_mrt<16>(c, a, st)); break;
-    default: RET(launch_mrt<32>(c, a, st)); break;
-  }
-  {
+  if (!c->vruns.empty()) {
+    RET(fd_var_runs(c, Hd, s_use, 0.0, rho2, xd, true, st));
+  } else {
+    RET(launch_mrt_u(c, a, st));
     LaunchScope ls(c, DP_KERNEL_FINISH, st);
     CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
   }
@@ -971,7 +1045,7 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
     return fail(DP_ERR_INVALID, "dims must be positive (n_sc=%d B=%d U=%d K=%d C=%d)", k.n_sc, k.B, k.U, k.K, k.C);
   if (k.K > 64) return fail(DP_ERR_INVALID, "K=%d > 64", k.K);
   if (k.world <= 0 || k.rank < 0 || k.rank >= k.world) return fail(DP_ERR_INVALID, "rank %d / world %d", k.rank, k.world);
-  if (k.B % k.C) return fail(DP_ERR_INVALID, "B=%d not divisible by C=%d (equal clusters, P:157)", k.B, k.C);
+  if (k.B % k.world) return fail(DP_ERR_INVALID, "B=%d not divisible by world=%d", k.B, k.world);
   if (k.C % k.world) return fail(DP_ERR_INVALID, "C=%d not divisible by world=%d", k.C, k.world);
   if (!(k.Es > 0.0) || !std::isfinite(k.Es)) return fail(DP_ERR_INVALID, "Es must be > 0");
   if (!(k.tau >= 0.0) || !std::isfinite(k.tau)) return fail(DP_ERR_INVALID, "tau must be >= 0");
@@ -981,8 +1055,10 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
     return fail(DP_ERR_INVALID, "DP_PD_SCATTER_GATHER needs n_sc=%d divisible by world=%d", k.n_sc, k.world);
   if (k.U != 4 && k.U != 8 && k.U != 16 && k.U != 32)
     return fail(DP_ERR_UNSUPPORTED, "U=%d: supported U are 4, 8, 16, 32", k.U);
-  const int S = k.B / k.C;
-  if (S < k.U && S != 4 && S != 8 && S != 16)   // FD branch B_c < U: fd_small.cuh
+  // equal split S = B / C (P:157 with w_c = 1/C); 0 when C does not divide B: the sizes then come
+  // from dp_set_clusters before any FD / MRT call
+  const int S = (k.B % k.C) ? 0 : k.B / k.C;
+  if (S && S < k.U && S != 4 && S != 8 && S != 16)   // FD branch B_c < U: fd_small.cuh
     return fail(DP_ERR_UNSUPPORTED, "B/C=%d < U=%d: the small-cluster branch supports B_c in {4, 8, 16}", S, k.U);
   const bool comm_on = k.world > 1 || (k.flags & DP_FLAG_FORCE_COMM);
   if (comm_on && !k.nccl_id) return fail(DP_ERR_INVALID, "nccl_id is required when world > 1 or DP_FLAG_FORCE_COMM");
@@ -998,8 +1074,8 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   c->S = S;
   // per-subcarrier PD kernels: split clusters into chunks (>= U rows) until the
   // CTA has >= 256 threads of SGs
-  int chunk = S;
-  if (S < k.U) {                        // small clusters: PD chunks span several clusters (>= U rows)
+  int chunk = S ? S : c->Bl;
+  if (S && S < k.U) {                        // small clusters: PD chunks span several clusters (>= U rows)
     chunk = c->Bl;
     for (int m = S; m < c->Bl; m += S)
       if (m >= k.U && c->Bl % m == 0) { chunk = m; break; }
@@ -1011,8 +1087,9 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   c->fdu_nw = next_pow2((c->Cl * k.U + 31) / 32);
   // FD fused: 4 warps, fewer if smem would not fit
   c->fd_nw = 4;
-  while (c->fd_nw > 1 && smem_fd_fused(k.U, S, k.K, c->fd_nw) > 100 * 1024) c->fd_nw >>= 1;
-  if (smem_fd_fused(k.U, S, k.K, c->fd_nw) > 227 * 1024) {
+  const int S_fd = S ? S : k.U;
+  while (c->fd_nw > 1 && smem_fd_fused(k.U, S_fd, k.K, c->fd_nw) > 100 * 1024) c->fd_nw >>= 1;
+  if (smem_fd_fused(k.U, S_fd, k.K, c->fd_nw) > 227 * 1024) {
     delete c;
     return fail(DP_ERR_UNSUPPORTED, "cluster tile S=%d x U=%d does not fit in shared memory", S, k.U);
   }
@@ -1141,6 +1218,68 @@ int dp_comm_ledger(dp_ctx *c, long long *floats, int reset) {
   return DP_OK;
 }
 
+int dp_set_clusters(dp_ctx *c, const int *B_c, const double *power, const double *tau) {
+  g_err.clear();
+  if (!c) return fail(DP_ERR_INVALID, "ctx is NULL");
+  const dp_config &k = c->cfg;
+  const int C = k.C;
+  std::vector<int> sz(C);
+  std::vector<double> w(C), t(C);
+  long long sum = 0;
+  double wsum = 0.0;
+  bool equal = true;
+  if (!B_c && c->S == 0) return fail(DP_ERR_INVALID, "B=%d not divisible by C=%d: B_c is required", k.B, C);
+  for (int i = 0; i < C; ++i) {
+    sz[i] = B_c ? B_c[i] : c->S;
+    w[i] = power ? power[i] : 1.0 / C;
+    t[i] = tau ? tau[i] : k.tau;
+    if (sz[i] <= 0) return fail(DP_ERR_INVALID, "B_c[%d]=%d must be positive", i, sz[i]);
+    if (!(w[i] > 0.0) || !std::isfinite(w[i])) return fail(DP_ERR_INVALID, "power[%d] must be > 0", i);
+    if (!(t[i] >= 0.0) || !std::isfinite(t[i])) return fail(DP_ERR_INVALID, "tau[%d] must be >= 0", i);
+    if (sz[i] < k.U && sz[i] != 4 && sz[i] != 8 && sz[i] != 16)
+      return fail(DP_ERR_UNSUPPORTED, "B_c[%d]=%d < U=%d: the small-cluster branch supports B_c in {4, 8, 16}", i,
+                  sz[i], k.U);
+    if (sz[i] >= k.U && !(c->use_tc && k.U == 32 && sz[i] == 32 && k.K <= 16) &&
+        smem_fd_fused(k.U, sz[i], k.K, c->fd_nw) > 227 * 1024)
+      return fail(DP_ERR_UNSUPPORTED, "B_c[%d]=%d: the FD tile needs more than 227 KB of shared memory", i, sz[i]);
+    sum += sz[i];
+    wsum += w[i];
+    equal = equal && sz[i] == c->S && std::fabs(w[i] - 1.0 / C) <= 1e-12 && t[i] == k.tau;
+  }
+  if (sum != k.B) return fail(DP_ERR_INVALID, "sum of B_c = %lld != B = %d", sum, k.B);
+  if (std::fabs(wsum - 1.0) > 1e-9) return fail(DP_ERR_INVALID, "sum of power shares = %.12g != 1", wsum);
+  const int c0 = k.rank * c->Cl;
+  long long local = 0;
+  for (int i = c0; i < c0 + c->Cl; ++i) local += sz[i];
+  if (local != c->Bl)
+    return fail(DP_ERR_INVALID, "rank %d: its clusters hold %lld antennas, need B/world = %d", k.rank, local, c->Bl);
+  std::vector<dp_ctx::VarRun> runs;
+  int off = 0;
+  for (int i = c0; i < c0 + c->Cl; ++i) {
+    if (!runs.empty()) {
+      auto &r = runs.back();
+      if (r.S == sz[i] && r.w == w[i] && r.tau == t[i]) {
+        ++r.len;
+        off += sz[i];
+        continue;
+      }
+    }
+    runs.push_back({i - c0, 1, sz[i], off, w[i], t[i]});
+    off += sz[i];
+  }
+  if (!equal && (int)runs.size() > dpk::VAR_MAX_RUNS)
+    return fail(DP_ERR_UNSUPPORTED, "%d runs of equal clusters > %d", (int)runs.size(), dpk::VAR_MAX_RUNS);
+  if (equal) {
+    c->vruns.clear();
+    c->vsizes.clear();
+  } else {
+    c->vruns = runs;
+    c->vsizes = sz;
+  }
+  if (c->prepared == 1) c->prepared = -1;                 // a cached FD W no longer matches
+  return DP_OK;
+}
+
 int dp_finalize(dp_ctx *c) {
   if (!c) return DP_OK;
   cudaSetDevice(c->cfg.device);
@@ -1166,6 +1305,8 @@ int dp_debug_gram(dp_ctx *c, const dp_c32 *H, int per_cluster, dp_c32 *G, void *
   a.H = reinterpret_cast<const float2 *>(H);
   a.Gout = reinterpret_cast<float2 *>(G);
   if (per_cluster) {
+    RET(need_split(c));
+    if (!c->vruns.empty()) return fail(DP_ERR_UNSUPPORTED, "dp_debug_gram per cluster: unequal clusters");
     a.S = c->S;
     a.nchunks = c->Cl;
     if (fd_tc_ok(c, a)) RET(launch_fd_tc_kc(c, a, st));   // the FD path's own (tensor-core) Gram
@@ -1201,6 +1342,8 @@ int dp_debug_solve(dp_ctx *c, const dp_c32 *G, int groups, const dp_c32 *s, doub
 // prepare continues as from the Gram kernel's output.
 int prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G, double N0, double rho2, cudaStream_t st) {
   const dp_config &k = c->cfg;
+  if (fd) RET(need_split(c));
+  if (fd && !c->vruns.empty()) return fail(DP_ERR_UNSUPPORTED, "prepare/apply: unequal clusters run fused only");
   const int groups = fd ? c->Cl : 1;
   const size_t nG = (size_t)k.n_sc * groups * dpk::npacked(k.U);
   CK(cudaMemcpyAsync(c->G, G, nG * sizeof(float2), cudaMemcpyDeviceToDevice, st));
@@ -1263,7 +1406,9 @@ int dp_prepare_fd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
   if (!is_device_ptr(H)) return fail(DP_ERR_INVALID, "dp_prepare_fd takes device pointers");
   if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
   if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");
+  RET(need_split(c));
   if (c->S < c->cfg.U) return fail(DP_ERR_UNSUPPORTED, "prepare/apply: FD branch B_c < U runs fused only");
+  if (!c->vruns.empty()) return fail(DP_ERR_UNSUPPORTED, "prepare/apply: unequal clusters run fused only");
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(c->cfg.device));
   const dp_config &k = c->cfg;
@@ -1294,6 +1439,7 @@ int dp_prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G_packed, double N0, d
   if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
   if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");
   if (fd != 0 && fd != 1) return fail(DP_ERR_INVALID, "fd must be 0 (PD) or 1 (FD)");
+  if (fd) RET(need_split(c));
   if (fd && c->S < c->cfg.U) return fail(DP_ERR_UNSUPPORTED, "prepare/apply: FD branch B_c < U runs fused only");
   CK(cudaSetDevice(c->cfg.device));
   return prepare_from_gram(c, fd, G_packed, N0, rho2, (cudaStream_t)stream);

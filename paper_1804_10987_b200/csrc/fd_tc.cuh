@@ -215,10 +215,11 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     tc::fence_mbar_init();
     // H is an input of the call (no predecessor kernel writes it): its tiles are fetched
     // before griddepcontrol.wait, overlapping the previous kernel's tail
-    for (int p = 0; p < np; ++p) {
+    for (int p = 0; p < np; ++p) {   // cluster (sc, cl) = rows sc Bl + 32 cl (Bl > 32 nchunks: unequal runs)
+      const int pp = p0 + p, row = (pp / a.nchunks) * a.Bl + (pp % a.nchunks) * 32;
       tc::mbar_arrive_expect_tx(&tile_full[p], FDT_TILE);
-      tc::tma_load_2d(tile(p), &tmH, 0, (p0 + p) * 32, &tile_full[p]);
-      tc::tma_load_2d(tile(p) + 4096, &tmH, 32, (p0 + p) * 32, &tile_full[p]);
+      tc::tma_load_2d(tile(p), &tmH, 0, row, &tile_full[p]);
+      tc::tma_load_2d(tile(p) + 4096, &tmH, 32, row, &tile_full[p]);
     }
     // and the tiles of the CTA that will most likely reuse this SM slot go to L2
     const int pn = p0 + 4 * a.pf_dist;

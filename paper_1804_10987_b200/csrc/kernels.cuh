@@ -749,6 +749,7 @@ struct Args {
   int fin_inv_beta;     // 1: fin[.][0] = sum 1/beta ; 0: fin[.][0] = 0 (PD ranks != 0)
   int pf_dist;          // fd_tc: L2-prefetch the tiles of CTA blockIdx.x + pf_dist (0: off)
   int fold;             // fd_tc: per-subcarrier scalars in-kernel (CTAs per subcarrier; 0 = finish kernel)
+  int hrow_off;         // host only: H rows before a.H in its allocation (unequal-cluster runs; TMA extent)
 };
 
 // Programmatic dependent launch: wait for the predecessor grid's completion (and
@@ -797,10 +798,11 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   float2 *tile = smem + (size_t)sg * (tile_sz + scr_sz);
   float2 *scr = tile + tile_sz;
   {
-    const float2 *g = a.H + (size_t)p0 * tile_sz;
-    for (int q = 0; q < np; ++q)
-      load_tile_async<U>(smem + (size_t)q * (tile_sz + scr_sz), g + (size_t)q * tile_sz, a.S, threadIdx.x,
-                         blockDim.x);
+    for (int q = 0; q < np; ++q) {   // cluster (sc, cl) = rows sc Bl + cl S of H (Bl > nchunks S: unequal runs)
+      const int pq = p0 + q;
+      const float2 *g = a.H + ((size_t)(pq / a.nchunks) * a.Bl + (size_t)(pq % a.nchunks) * a.S) * U;
+      load_tile_async<U>(smem + (size_t)q * (tile_sz + scr_sz), g, a.S, threadIdx.x, blockDim.x);
+    }
     cp_async_wait_all();
     __syncthreads();
   }
@@ -1140,6 +1142,37 @@ __global__ void __launch_bounds__(128) fd_finish_kernel(Args a) {
   pdl_wait();
   const int sc = blockIdx.x * blockDim.x + threadIdx.x;
   if (sc < a.n_sc) finish_sc(a, sc);
+}
+
+// ================================================================== FD finish, unequal clusters
+// Clusters of unequal size / power / tau (Eq. 9) run as maximal runs of equal
+// parameters, one FD launch per run; run r wrote beta and power partials of its len[r]
+// clusters to vb / vp + n_sc cl0[r] in [sc][len[r]] layout.  Per subcarrier, in ascending
+// cluster order (the order of finish_sc): beta_c -> a.beta[sc][Cl], fin = {sum_c 1/beta_c,
+// sum_c power_c}.
+constexpr int VAR_MAX_RUNS = 64;
+struct VarRuns {
+  int n, Cl;
+  const float *vb, *vp;
+  int cl0[VAR_MAX_RUNS], len[VAR_MAX_RUNS];
+};
+__global__ void __launch_bounds__(128) fd_var_finish_kernel(Args a, VarRuns r) {
+  pdl_trigger();
+  pdl_wait();
+  const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sc >= a.n_sc) return;
+  float ib = 0.f, p = 0.f;
+  for (int i = 0; i < r.n; ++i) {
+    const size_t o = (size_t)a.n_sc * r.cl0[i] + (size_t)sc * r.len[i];
+    for (int j = 0; j < r.len[i]; ++j) {
+      const float b = __ldcg(r.vb + o + j);
+      a.beta[(size_t)sc * r.Cl + r.cl0[i] + j] = b;
+      ib += 1.f / b;
+      p += __ldcg(r.vp + o + j);
+    }
+  }
+  a.fin[2 * sc] = ib;
+  a.fin[2 * sc + 1] = p;
 }
 
 // which: 1 -> rx = 1 / fin[.][0] ; 2 -> power = fin[.][1]

@@ -64,7 +64,7 @@ def _cfg(**kw):
 
 @pytest.mark.parametrize("kw,code", [
     (dict(n_sc=0), L.DP_ERR_INVALID),
-    (dict(B=15), L.DP_ERR_INVALID),            # B % C
+    (dict(B=15, world=2, C=2), L.DP_ERR_INVALID),   # B % world
     (dict(world=2, rank=0, C=3, B=18), L.DP_ERR_INVALID),   # C % world
     (dict(Es=0.0), L.DP_ERR_INVALID),
     (dict(tau=-1.0), L.DP_ERR_INVALID),

@@ -411,3 +411,76 @@ def test_mrt_fd_pins():
             P = np.conj(Hc) / bc[w, c]                    # P_c = H_c^H / beta_c, [S][U]
             assert 0.8 * np.trace(P.conj().T @ P).real == pytest.approx(1.5 / C, rel=1e-12)
             assert np.allclose(x[w, :, c * S:(c + 1) * S], (P @ s[w].T).T, atol=1e-12)
+
+
+# --------------------------------------------------------------------------- unequal clusters (§8 f3)
+VAR_CASES = [
+    # (U, sizes, power shares, tau_c): B_c < U (small branch), = U, > U; unequal power and tau
+    (8, [4, 8, 20, 16], [0.1, 0.2, 0.4, 0.3], [0.125, 0.5, 1.0, 0.25]),
+    (4, [4, 12, 8], [0.5, 0.25, 0.25], [0.125, 0.125, 2.0]),
+]
+
+
+@pytest.mark.parametrize("U,sizes,power,tau", VAR_CASES)
+def test_fd_var_cluster_is_local_wf(U, sizes, power, tau):
+    """Unequal clusters (P:157 B_c = w_c B) with power shares rho_c^2 and tau_c (Eq. 9):
+    cluster c == centralized WF on (H_c, N0' = tau_c N0, rho'^2 = rho_c^2) (Theorem 1 route of
+    oracle.wf); the equal split reduces to oracle.fd."""
+    rng = np.random.default_rng(U + len(sizes))
+    n_sc, K, N0, rho2, Es = 3, 5, 0.1, 1.5, 0.8
+    B = sum(sizes)
+    H = rand_h(rng, n_sc, B, U)
+    s = rand_s(rng, n_sc, K, U)
+    x, b_c = oracle.fd_var(H, s, sizes, N0, rho2, Es, power=power, tau=tau)
+    off = 0
+    for c, S in enumerate(sizes):
+        x_c, b = oracle.wf(H[:, off:off + S], s, tau[c] * N0, power[c] * rho2, Es)
+        assert rel(x[:, :, off:off + S], x_c) <= 1e-11
+        assert np.max(np.abs(b_c[:, c] / b - 1)) <= 1e-11
+        off += S
+    C = 4
+    xe, be = oracle.fd_var(H[:, :C * U], s, [U] * C, N0, rho2, Es, tau=0.3)
+    xr, br = oracle.fd(H[:, :C * U], s, C, N0, rho2, Es, tau=0.3)
+    assert rel(xe, xr) <= 1e-13 and np.max(np.abs(be / br - 1)) <= 1e-13
+
+
+@pytest.mark.parametrize("U,sizes,power,tau", VAR_CASES)
+def test_fd_var_power_split_and_library(U, sizes, power, tau):
+    """Per-cluster power Es ||P_c||_F^2 = rho_c^2, so sum_c = rho^2 (Eq. 2); and P_c
+    against numpy: Q_c = H_c^H (H_c H_c^H + kappa_c I)^-1 with kappa_c = tau_c U N0 / rho_c^2."""
+    rng = np.random.default_rng(7 * U)
+    N0, rho2, Es = 0.2, 2.0, 1.0
+    B = sum(sizes)
+    H = rand_h(rng, 1, B, U)
+    P, _ = P_of(lambda H_, s: oracle.fd_var(H_, s, sizes, N0, rho2, Es, power=power, tau=tau), H[0])
+    off = 0
+    for c, S in enumerate(sizes):
+        Pc = P[off:off + S]
+        assert Es * np.linalg.norm(Pc) ** 2 == pytest.approx(power[c] * rho2, rel=1e-12)
+        Hp = H[0, off:off + S].T                                   # H_c^paper, U x B_c
+        kc = tau[c] * U * N0 / (power[c] * rho2)
+        Qc = Hp.conj().T @ np.linalg.solve(Hp @ Hp.conj().T + kc * np.eye(U), np.eye(U))
+        assert rel(Pc, Qc / np.sqrt(Es * np.linalg.norm(Qc) ** 2 / (power[c] * rho2))) < 1e-10
+        off += S
+    assert Es * np.linalg.norm(P) ** 2 == pytest.approx(rho2, rel=1e-12)
+
+
+def test_mrt_fd_var_pins():
+    """MRT with unequal clusters: x_c = H_c^H s / beta_c, Es ||P_c||_F^2 = rho_c^2 (numpy), and the
+    equal split reduces to oracle.mrt_fd."""
+    rng = np.random.default_rng(11)
+    U, sizes, power = 4, [8, 4, 12], [0.2, 0.5, 0.3]
+    B, K = sum(sizes), 3
+    H = rand_h(rng, 2, B, U)
+    s = rand_s(rng, 2, K, U)
+    x, bc = oracle.mrt_fd_var(H, s, sizes, rho2=1.5, Es=0.8, power=power)
+    off = 0
+    for c, S in enumerate(sizes):
+        for w in range(2):
+            P = np.conj(H[w, off:off + S]) / bc[w, c]
+            assert 0.8 * np.linalg.norm(P) ** 2 == pytest.approx(power[c] * 1.5, rel=1e-12)
+            assert np.allclose(x[w, :, off:off + S], (P @ s[w].T).T, atol=1e-12)
+        off += S
+    xe, be = oracle.mrt_fd_var(H[:, :12], s, [4, 4, 4], rho2=1.5)
+    xr, br = oracle.mrt_fd(H[:, :12], s, 3, rho2=1.5)
+    assert rel(xe, xr) <= 1e-13 and np.max(np.abs(be / br - 1)) <= 1e-13
