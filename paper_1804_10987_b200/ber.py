@@ -57,11 +57,14 @@ class BerRun:
             self._pre[C] = Precoder(self.n_sc, self.B, self.U, self.K, C, tau=self.tau)
         return self._pre[C]
 
-    def point(self, mode: str, C: int, snr_db: float, frames: int, frame0: int = 0):
+    def point(self, mode: str, C: int, snr_db: float, frames: int, frame0: int = 0, sizes=None, power=None,
+              taus=None):
         """Bit errors and bits for `frames` frames; mode "pd" (= centralized WF), "fd" or
-        "mrt" (fully-distributed MRT, the Fig. 2 baseline)."""
+        "mrt" (fully-distributed MRT, the Fig. 2 baseline).  sizes / power / taus: an unequal
+        partition for FD / MRT (dp_set_clusters; None = equal split, 1/C, the run's tau)."""
         N0 = 10.0 ** (-snr_db / 10.0)       # rho^2 = Es = 1 (reading R10)
         pre = self._precoder(C)
+        pre.set_clusters(sizes, power, taus)
         errors = torch.zeros(1, dtype=torch.int64, device="cuda")
         rx = torch.empty(self.n_sc, dtype=torch.float32, device="cuda")
         for f in range(frame0, frame0 + frames):

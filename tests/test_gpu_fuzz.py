@@ -51,3 +51,38 @@ def test_random_shapes(seed):
     assert rel_l2(x_pd, xr_pd) <= REL_TOL, (case, rel_l2(x_pd, xr_pd))
     assert rel_l2(x_fd, xr_fd) <= REL_TOL, (case, rel_l2(x_fd, xr_fd))
     assert np.max(np.abs(rx_fd / oracle.rx_scale_fd(br) - 1)) <= REL_TOL, case
+
+
+def _var_case(seed: int):
+    """Random unequal partition: sizes from the supported set, Dirichlet power shares,
+    per-cluster tau_c; C need not divide B."""
+    rng = np.random.default_rng(5000 + seed)
+    U = int(rng.choice([4, 8, 16, 32]))
+    allowed = [U, U + 8, 2 * U, 3 * U] + [b for b in (4, 8, 16) if b < U]
+    C = int(rng.integers(2, 9))
+    sizes = [int(rng.choice(allowed)) for _ in range(C)]
+    if rng.random() < 0.5:                            # long runs of equal clusters too
+        sizes = sorted(sizes)
+    power = rng.dirichlet(np.full(C, 2.0)).tolist()
+    tau = [float(v) for v in rng.choice([0.125, 0.25, 0.5, 1.0], size=C)]
+    K = int(rng.integers(1, 17))
+    n_sc = int(rng.choice([1, int(rng.integers(2, 41)), int(rng.integers(2, 41))]))
+    snr = float(rng.uniform(0.0, 15.0))
+    return U, sizes, power, tau, K, n_sc, snr
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_unequal_clusters(seed):
+    U, sizes, power, tau, K, n_sc, snr = _var_case(seed)
+    B, C = sum(sizes), len(sizes)
+    f = synth.make_frame(90 + seed, n_sc, B, U, K, 16)
+    N0 = synth.n0_from_snr_db(snr)
+    with Precoder(n_sc, B, U, K, C) as pre:
+        pre.set_clusters(sizes, power, tau)
+        x = pre.precode_fd(torch.from_numpy(f.H).cuda(), torch.from_numpy(f.s).cuda(), N0, 1.0).cpu().numpy()
+        rx = pre.read_scalars("rx").cpu().numpy()
+        assert pre.status() == 0
+    xr, br = oracle.fd_var(f.H, f.s, sizes, N0, power=power, tau=tau)
+    case = dict(U=U, sizes=sizes, K=K, n_sc=n_sc, snr=round(snr, 1))
+    assert rel_l2(x, xr) <= REL_TOL, (case, rel_l2(x, xr))
+    assert np.max(np.abs(rx / oracle.rx_scale_fd(br) - 1)) <= REL_TOL, case
