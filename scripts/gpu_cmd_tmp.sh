@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-DP_SOLVE_SG=1 timeout 300 ncu --set full --import-source on --clock-control none -k regex:"solve_kernel" -s 2 -c 1 -o gpurun_out/k_solve_sg python bench.py --profile-run --steps 3 --warmup 2 --mode pd > gpurun_out/ncu37.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_fuzz.py tests/test_gpu_unequal.py tests/test_ber.py -x -q > gpurun_out/pytest_fuzz.txt 2>&1
+echo "rc=$?" >> gpurun_out/pytest_fuzz.txt
+timeout 900 python scripts/ber_partition.py --frames 20 --out gpurun_out/ber_partition.json > gpurun_out/ber_partition.log 2>&1
