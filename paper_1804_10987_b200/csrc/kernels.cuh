@@ -798,10 +798,17 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   float2 *tile = smem + (size_t)sg * (tile_sz + scr_sz);
   float2 *scr = tile + tile_sz;
   {
-    for (int q = 0; q < np; ++q) {   // cluster (sc, cl) = rows sc Bl + cl S of H (Bl > nchunks S: unequal runs)
-      const int pq = p0 + q;
-      const float2 *g = a.H + ((size_t)(pq / a.nchunks) * a.Bl + (size_t)(pq % a.nchunks) * a.S) * U;
-      load_tile_async<U>(smem + (size_t)q * (tile_sz + scr_sz), g, a.S, threadIdx.x, blockDim.x);
+    if (a.Bl == a.nchunks * a.S) {   // clusters contiguous in H: problem p at p S rows
+      const float2 *g = a.H + (size_t)p0 * tile_sz;
+      for (int q = 0; q < np; ++q)
+        load_tile_async<U>(smem + (size_t)q * (tile_sz + scr_sz), g + (size_t)q * tile_sz, a.S, threadIdx.x,
+                           blockDim.x);
+    } else {                         // a run of unequal clusters: cluster (sc, cl) at rows sc Bl + cl S
+      for (int q = 0; q < np; ++q) {
+        const int pq = p0 + q;
+        const float2 *g = a.H + ((size_t)(pq / a.nchunks) * a.Bl + (size_t)(pq % a.nchunks) * a.S) * U;
+        load_tile_async<U>(smem + (size_t)q * (tile_sz + scr_sz), g, a.S, threadIdx.x, blockDim.x);
+      }
     }
     cp_async_wait_all();
     __syncthreads();
