@@ -378,8 +378,11 @@ int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
     static const int nw_env = getenv("DP_SOLVE_NW") ? atoi(getenv("DP_SOLVE_NW")) : 4;
     if (!sg_only) {                                                  // 4 (or 2) warps per problem (solve_mw.cuh)
       const int NW = nw_env == 2 ? 2 : 4;
-      const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KC, NW) * sizeof(float2);
-      auto kern = NW == 4 ? dpk::solve_mw_kernel<KC, 4> : dpk::solve_mw_kernel<KC, 2>;
+      // whitening in symbol chunks of at most 8: at 9 CTAs / SM (56 registers) 14 or 16
+      // accumulators spilled
+      constexpr int KS = KC > 8 ? KC / 2 : KC;
+      const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KS, NW) * sizeof(float2);
+      auto kern = NW == 4 ? dpk::solve_mw_kernel<KS, 4> : dpk::solve_mw_kernel<KS, 2>;
       CK(set_smem(kern, sm));
       LaunchScope ls(c, DP_KERNEL_SOLVE, st);
       CK(launch_pdl(kern, dim3((nprob + 4 / NW - 1) / (4 / NW)), dim3(dpk::SMW_THREADS), sm, st, a));
