@@ -87,6 +87,7 @@ def test_null_arguments():
     assert L.lib().dp_init(None, None) == L.DP_ERR_INVALID
     assert L.lib().dp_precode_pd(None, None, None, 0.1, 1.0, None, None) == L.DP_ERR_INVALID
     assert L.lib().dp_precode_fd(None, None, None, 0.1, 1.0, None, None) == L.DP_ERR_INVALID
+    assert L.lib().dp_set_clusters(None, None, None, None) == L.DP_ERR_INVALID
     assert L.lib().dp_finalize(None) == L.DP_OK
     assert L.lib().dp_get_unique_id(None) == L.DP_ERR_INVALID
 
