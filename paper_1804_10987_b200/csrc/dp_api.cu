@@ -955,7 +955,8 @@ using DevFn = int (*)(dp_ctx *, const float2 *, const float2 *, double, double, 
 int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c32 *s, double N0, double rho2,
                    dp_c32 *x, cudaStream_t st) {
   const dp_config k = c->cfg;
-  const int nch = std::min(8, k.n_sc);
+  static const int nch_env = getenv("DP_HOST_CHUNKS") ? atoi(getenv("DP_HOST_CHUNKS")) : 8;
+  const int nch = std::max(1, std::min(nch_env, k.n_sc));
   const size_t rowH = (size_t)c->Bl * k.U, rowS = (size_t)k.K * k.U, rowX = (size_t)k.K * c->Bl;
   if (!c->h_dev) {
     RET(alloc((void **)&c->h_dev, (size_t)k.n_sc * rowH * 8));
