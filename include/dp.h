@@ -20,12 +20,14 @@
  *       beta = sqrt(Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)) (Lemma 1, Eq. 6) ;
  *       z_k = A^{-1} s_k / beta ; x_{c,k} = H_c^H z_k.
  *   FD-WF (Sec. III-C):  per cluster, the same chain on H_c alone
- *       with rho_c^2 = rho^2/C and kappa_c = tau U N0/rho_c^2 (Eq. 9).
+ *       with rho_c^2 = rho^2/C and kappa_c = tau U N0/rho_c^2 (Eq. 9)
+ *       (per-cluster rho_c^2 and tau_c through dp_set_clusters).
  *
  * ---------------------------------------------------------------- layouts
  * dp_c32 is an interleaved complex float (== cuComplex == torch.complex64).
  * Antennas are numbered b = 0..B-1; cluster c owns antennas [c*S, (c+1)*S),
- * S = B/C (equal split).  Rank r of `world` owns clusters
+ * S = B/C (equal split; dp_set_clusters sets unequal sizes B_c, cluster c
+ * then starting at sum_{c' < c} B_c').  Rank r of `world` owns clusters
  * [r*C/world, (r+1)*C/world), i.e. the contiguous antenna block
  * [r*B/world, (r+1)*B/world) — "one GPU per cluster" with the
  * cluster count C decoupled from the GPU count.

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-for n in 3 4 6 8; do
-DP_HOST_CHUNKS=$n timeout -s KILL 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/e2e_$n.txt 2>&1
-done
+timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 10 --warmup 3 > gpurun_out/torchrun1.txt 2>&1
+echo "rc=$?" >> gpurun_out/torchrun1.txt
