@@ -26,6 +26,12 @@
 #pragma once
 #include "tcgen05.cuh"
 
+// diagnostics only (scripts, never the shipped build): 1 = no UMMAs, 2 = no UMMAs and no residual math,
+// 3 = 2 and no epilogue work (TMEM load, staging, G stores)
+#ifndef DP_GRAM_DIAG
+#define DP_GRAM_DIAG 0
+#endif
+
 namespace dpk {
 
 // U = 32: 2 atoms of 32 reals per antenna row, M = 128, N = 64 (D rows = TMEM lanes);
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(GT2<CH, U>::THREADS, 1) gram_tc2_kernel(const 
 #pragma unroll
           for (int t = 0; t < CH / 8; ++t) {                 // antennas 8t .. 8t+7
             const uint64_t dsc = smem_desc_mn_sw128b32(base + 1024 * t, T::BOX, 512);
-            tc::mma_tf32(d, dsc, dsc, IDESC, (c > 0 || t > 0) ? 1u : 0u);
+            if (DP_GRAM_DIAG < 1) tc::mma_tf32(d, dsc, dsc, IDESC, (c > 0 || t > 0) ? 1u : 0u);
           }
           tc::mma_commit(&stage_free[s]);
           if (++s == T::NS) { s = 0; ph ^= 1; }
@@ -126,8 +132,8 @@ __global__ void __launch_bounds__(GT2<CH, U>::THREADS, 1) gram_tc2_kernel(const 
         uint8_t *st = sm + (size_t)s * T::STAGE;
         const uint4 *src = reinterpret_cast<const uint4 *>(st);
         uint4 *dst = reinterpret_cast<uint4 *>(st + T::NA * T::BOX);
-        constexpr int NV = T::NA * T::BOX / 16 / 128;
-        uint4 v[NV];
+        constexpr int NV = (DP_GRAM_DIAG >= 2) ? 0 : T::NA * T::BOX / 16 / 128;
+        uint4 v[NV > 0 ? NV : 1];
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = src[ptid + 128 * i];
 #pragma unroll
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(GT2<CH, U>::THREADS, 1) gram_tc2_kernel(const 
       };
       float2 *out = a.Gout + (size_t)item * npacked(U);
 #pragma unroll 2
-      for (int e = tid; e < U * U; e += 128) {
+      for (int e = tid; e < (DP_GRAM_DIAG >= 3 ? 0 : U * U); e += 128) {
         const int u = e / U, v = e % U;
         if (u <= v) {
           const float gr = P(2 * u, 2 * v) + P(2 * u + 1, 2 * v + 1);
