@@ -484,3 +484,24 @@ def test_mrt_fd_var_pins():
     xe, be = oracle.mrt_fd_var(H[:, :12], s, [4, 4, 4], rho2=1.5)
     xr, br = oracle.mrt_fd(H[:, :12], s, 3, rho2=1.5)
     assert rel(xe, xr) <= 1e-13 and np.max(np.abs(be / br - 1)) <= 1e-13
+
+
+def test_fd_var_closed_form_repeated_identity_blocks():
+    """Closed form for unequal clusters: H_c^paper = a_c [I_U, .., I_U] (m_c blocks, B_c = m_c U) gives
+    H_c H_c^H = m_c |a_c|^2 I, Q_c = H_c^H / (m_c |a_c|^2 + kappa_c), and by P:217
+    x_c = (conj(a_c)/|a_c|) [s; ..; s] sqrt(rho_c^2 / (m_c U Es)) for every kappa_c (tau_c, N0)."""
+    U, K, Es, rho2, N0 = 4, 3, 0.9, 1.7, 0.3
+    a = [0.6 - 0.8j, 2.0 + 0.0j, -0.3 + 0.4j]
+    m = [1, 3, 2]
+    power = [0.2, 0.5, 0.3]
+    tau = [0.125, 1.0, 4.0]
+    Ht = np.concatenate([a[c] * np.concatenate([np.eye(U)] * m[c], axis=0) for c in range(3)], axis=0)[None]
+    rng = np.random.default_rng(3)
+    s = rand_s(rng, 1, K, U)
+    sizes = [mc * U for mc in m]
+    x, _ = oracle.fd_var(Ht, s, sizes, N0, rho2, Es, power=power, tau=tau)
+    off = 0
+    for c in range(3):
+        want = np.conj(a[c]) / abs(a[c]) * np.tile(s[0], (1, m[c])) * np.sqrt(power[c] * rho2 / (m[c] * U * Es))
+        assert np.allclose(x[0, :, off:off + sizes[c]], want, atol=1e-12)
+        off += sizes[c]
