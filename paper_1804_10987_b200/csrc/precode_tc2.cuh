@@ -28,6 +28,12 @@
 //   warps 0-3  epilogue: TMEM lane quarter -> x rows (coalesced: one antenna per lane),
 //              the subcarrier's power, and its per-subcarrier scalars (fin).
 #pragma once
+
+// diagnostics only (scripts/gram_diag.sh builds, never the shipped build): 1 = no UMMAs, 2 = no UMMAs
+// and no residual math, 3 = 2 and no x stores
+#ifndef DP_PC2_DIAG
+#define DP_PC2_DIAG 0
+#endif
 #include "tcgen05.cuh"
 
 namespace dpk {
@@ -119,8 +125,10 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
           for (int t = 0; t < 8; ++t) {               // K = 64 reals in 8 steps of 8
             const uint32_t koff = (uint32_t)(t >> 2) * PC2_BOX + (uint32_t)(t & 3) * 32;
             const uint64_t zd = tc::smem_desc(zo + t * 2 * 64 * 16, 64 * 16, 128);
-            tc::mma_tf32(d, tc::smem_desc_sw128(hb + koff, 1024), zd, ID64, t > 0 ? 1u : 0u);
-            tc::mma_tf32(d, tc::smem_desc_sw128(hs + koff, 1024), zd, ID32, 1u);
+            if (DP_PC2_DIAG < 1) {
+              tc::mma_tf32(d, tc::smem_desc_sw128(hb + koff, 1024), zd, ID64, t > 0 ? 1u : 0u);
+              tc::mma_tf32(d, tc::smem_desc_sw128(hs + koff, 1024), zd, ID32, 1u);
+            }
           }
           tc::mma_commit(&stage_free[s]);
           tc::mma_commit(&hs_free[b]);
@@ -172,8 +180,8 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
         uint8_t *st = sm + (size_t)s * PC2_STAGE;
         const uint4 *src = reinterpret_cast<const uint4 *>(st);
         uint4 *dst = reinterpret_cast<uint4 *>(hsb + (size_t)hbuf * PC2_STAGE);
-        constexpr int NV = 2 * PC2_BOX / 16 / 128;      // 16 vectors per thread
-        uint4 v[NV];
+        constexpr int NV = DP_PC2_DIAG >= 2 ? 0 : 2 * PC2_BOX / 16 / 128;      // 16 vectors per thread
+        uint4 v[NV > 0 ? NV : 1];
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = src[ptid + 128 * i];
 #pragma unroll
@@ -212,7 +220,7 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
         float2 *x = a.x + (size_t)item * a.K * a.Bl + blk * PC2_ROWS + 32 * warp + lane;
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (k < a.K) {
+          if (k < a.K && DP_PC2_DIAG < 3) {
             const float re = v[0][k] + v[2][k], im = v[1][k] + v[3][k];
             x[(size_t)k * a.Bl] = make_float2(re, im);
             pw = fmaf(re, re, fmaf(im, im, pw));
