@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time for cpu_baseline")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no JSON extras)")
+    ap.add_argument("--cluster-sizes", default="", help="comma list of C unequal cluster sizes B_c (dp_set_clusters, "
+                    "P:157); FD only, power shares B_c / B")
     ap.add_argument("--eager", action="store_true", help="launch the timed steps eagerly (default: replay a CUDA "
                     "graph captured from the same K steps; host launch overhead out of the timed region)")
     return ap.parse_args()
@@ -235,6 +237,11 @@ def main():
     pre_prof = Precoder(cfg.n_sc, cfg.B, cfg.U, cfg.K, cfg.C, rank=rank, world=world, device=local, tau=cfg.tau,
                         pd_topology=args.pd_topology, s_on_all_ranks=(world == 1), flags=flags | L.DP_FLAG_PROFILE,
                         nccl_id=D.bootstrap_nccl_id() if world > 1 else None)
+
+    sizes = [int(v) for v in args.cluster_sizes.split(",")] if args.cluster_sizes else None
+    if sizes:
+        for p_ in (pre, pre_prof):
+            p_.set_clusters(sizes, [b / cfg.B for b in sizes])
 
     # ---------------- resident rotating input sets (> 2x L2 in total)
     bf = bytes_frame(cfg, Bl)
@@ -482,6 +489,7 @@ def main():
                                    f"K={cfg.K} {cfg.M}-QAM SNR={cfg.snr_db} dB tau={cfg.tau}",
                        "step": "+".join(m.upper() + "-WF frame" for m in modes),
                        "bits_per_step": bits_step, "clusters_per_gpu": Cl,
+                       **({"cluster_sizes": sizes} if sizes else {}),
                        "parallelism": f"cluster-sharded x{world}" + ("" if world == 1 else f", PD {args.pd_topology}"),
                        "l2": f"{R} rotating resident input sets of {per_set / 2**20:.1f} MiB (> 2x L2)",
                        "path": "unfused (a)(b)(c)" if args.unfused else "fused single pass",

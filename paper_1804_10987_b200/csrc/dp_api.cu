@@ -107,6 +107,8 @@ struct dp_ctx {
   struct VarRun { int cl0, len, S, off; double w, tau; };
   std::vector<VarRun> vruns;
   std::vector<int> vsizes;   // all C cluster sizes (global) when set
+  cudaStream_t st_run[3] = {nullptr, nullptr, nullptr};   // concurrent runs (fork / join on events)
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   // last call
   int last_mode = -1;        // 0 pd, 1 fd
   int prepared = -1;         // W cached in G by dp_prepare_pd (0) / dp_prepare_fd (1); -1 none
@@ -718,7 +720,23 @@ int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, dou
   vr.vb = vb;
   vr.vp = vb + n;
   int rc = DP_OK;
+  // the runs touch disjoint H rows, x columns and scratch: up to 3 run on their own streams so
+  // their partial waves overlap (fork after the scratch allocation, join before the finish)
+  static const bool serial = getenv("DP_VAR_SERIAL") != nullptr;
+  const int nfork = serial ? 0 : std::min(vr.n, 3);
+  if (nfork > 1) {
+    if (!c->ev_fork) {
+      CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      for (int j = 0; j < 3; ++j) {
+        CK(cudaStreamCreateWithFlags(&c->st_run[j], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_join[j], cudaEventDisableTiming));
+      }
+    }
+    CK(cudaEventRecord(c->ev_fork, st));
+    for (int j = 0; j < nfork; ++j) CK(cudaStreamWaitEvent(c->st_run[j], c->ev_fork, 0));
+  }
   for (int i = 0; i < vr.n && rc == DP_OK; ++i) {
+    const cudaStream_t sr = nfork > 1 ? c->st_run[i % nfork] : st;
     const auto &r = c->vruns[i];
     const double rho_c2 = r.w * rho2;                     // rho_c^2 = w_c rho^2, sum_c w_c = 1
     Args a = base_args(c);
@@ -736,15 +754,20 @@ int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, dou
     a.fold = 0;
     vr.cl0[i] = r.cl0;
     vr.len[i] = r.len;
-    if (mrt) rc = launch_mrt_u(c, a, st);
-    else if (r.S < k.U) rc = launch_fd_small(c, a, st);
-    else if (fd_tc_ok(c, a)) rc = launch_fd_tc_kc(c, a, st);
-    else rc = dispatch<FdFused>(k.U, k.K, c, a, st);
+    if (mrt) rc = launch_mrt_u(c, a, sr);
+    else if (r.S < k.U) rc = launch_fd_small(c, a, sr);
+    else if (fd_tc_ok(c, a)) rc = launch_fd_tc_kc(c, a, sr);
+    else rc = dispatch<FdFused>(k.U, k.K, c, a, sr);
   }
+  if (nfork > 1)
+    for (int j = 0; j < nfork; ++j) {
+      CK(cudaEventRecord(c->ev_join[j], c->st_run[j]));
+      CK(cudaStreamWaitEvent(st, c->ev_join[j], 0));
+    }
   if (rc == DP_OK) {
     Args a = base_args(c);
     LaunchScope ls(c, DP_KERNEL_FINISH, st);
-    const cudaError_t e = launch_pdl(dpk::fd_var_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a, vr);
+    const cudaError_t e = launch_pdl(dpk::fd_var_finish_kernel, dim3((k.n_sc + 3) / 4), dim3(128), 0, st, a, vr);
     if (e != cudaSuccess) rc = fail(DP_ERR_CUDA, "fd_var_finish_kernel: %s", cudaGetErrorString(e));
   }
   CK(cudaFreeAsync(vb, st));
@@ -1293,6 +1316,11 @@ int dp_finalize(dp_ctx *c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->st_h2d) cudaStreamDestroy(c->st_h2d);
   if (c->st_d2h) cudaStreamDestroy(c->st_d2h);
+  for (int j = 0; j < 3; ++j) {
+    if (c->st_run[j]) cudaStreamDestroy(c->st_run[j]);
+    if (c->ev_join[j]) cudaEventDestroy(c->ev_join[j]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev};
   for (void *b : bufs)
     if (b) cudaFree(b);

@@ -1154,9 +1154,8 @@ __global__ void __launch_bounds__(128) fd_finish_kernel(Args a) {
 // ================================================================== FD finish, unequal clusters
 // Clusters of unequal size / power / tau (Eq. 9) run as maximal runs of equal
 // parameters, one FD launch per run; run r wrote beta and power partials of its len[r]
-// clusters to vb / vp + n_sc cl0[r] in [sc][len[r]] layout.  Per subcarrier, in ascending
-// cluster order (the order of finish_sc): beta_c -> a.beta[sc][Cl], fin = {sum_c 1/beta_c,
-// sum_c power_c}.
+// clusters to vb / vp + n_sc cl0[r] in [sc][len[r]] layout.  Per subcarrier: beta_c ->
+// a.beta[sc][Cl], fin = {sum_c 1/beta_c, sum_c power_c}.
 constexpr int VAR_MAX_RUNS = 64;
 struct VarRuns {
   int n, Cl;
@@ -1166,20 +1165,28 @@ struct VarRuns {
 __global__ void __launch_bounds__(128) fd_var_finish_kernel(Args a, VarRuns r) {
   pdl_trigger();
   pdl_wait();
-  const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per subcarrier, lane = cluster (strided); butterfly sums in a fixed order
+  const int sc = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (sc >= a.n_sc) return;
   float ib = 0.f, p = 0.f;
-  for (int i = 0; i < r.n; ++i) {
-    const size_t o = (size_t)a.n_sc * r.cl0[i] + (size_t)sc * r.len[i];
-    for (int j = 0; j < r.len[i]; ++j) {
-      const float b = __ldcg(r.vb + o + j);
-      a.beta[(size_t)sc * r.Cl + r.cl0[i] + j] = b;
-      ib += 1.f / b;
-      p += __ldcg(r.vp + o + j);
-    }
+  for (int c = lane; c < r.Cl; c += 32) {
+    int i = 0;
+    while (i + 1 < r.n && r.cl0[i + 1] <= c) ++i;       // run of cluster c
+    const size_t o = (size_t)a.n_sc * r.cl0[i] + (size_t)sc * r.len[i] + (c - r.cl0[i]);
+    const float b = __ldcg(r.vb + o);
+    a.beta[(size_t)sc * r.Cl + c] = b;
+    ib += 1.f / b;
+    p += __ldcg(r.vp + o);
   }
-  a.fin[2 * sc] = ib;
-  a.fin[2 * sc + 1] = p;
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    ib += __shfl_xor_sync(0xffffffffu, ib, m);
+    p += __shfl_xor_sync(0xffffffffu, p, m);
+  }
+  if (lane == 0) {
+    a.fin[2 * sc] = ib;
+    a.fin[2 * sc + 1] = p;
+  }
 }
 
 // which: 1 -> rx = 1 / fin[.][0] ; 2 -> power = fin[.][1]
