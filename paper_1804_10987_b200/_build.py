@@ -11,13 +11,16 @@ import glob
 import os
 import subprocess
 import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libdp.so")
-SOURCES = [os.path.join(CSRC, "dp_api.cu")]
+# one translation unit per kernel group (compiled in parallel, then linked)
+SOURCES = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 DEPS = SOURCES + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "dp.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -67,15 +70,34 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         return LIB
     inc, lib = nccl_dirs()
     libname = os.path.basename(sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0])
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-DDP_BUILD", *[f"-D{d}" for d in defines],
-           "-I", INCLUDE, "-I", CSRC, "-I", inc,
-           *SOURCES, "-o", LIB + ".tmp",
-           "-L", lib, f"-l:{libname}", "-Xlinker", f"-rpath,{lib}"]
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-fvisibility=hidden", "-DDP_BUILD", *[f"-D{d}" for d in defines],
+              "-I", INCLUDE, "-I", CSRC, "-I", inc]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        common.insert(1, "-Xptxas=-v")
+    tmp = tempfile.mkdtemp(prefix="dpbuild_")
+    objs = [os.path.join(tmp, os.path.basename(src)[:-3] + ".o") for src in SOURCES]
+
+    def compile_one(args):
+        src, obj = args
+        cmd = [*common, "-c", src, "-o", obj]
+        print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0 or verbose:
+            sys.stderr.write(r.stderr)
+        return r.returncode
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        rcs = list(ex.map(compile_one, zip(SOURCES, objs)))
+    if any(rcs):
+        raise subprocess.CalledProcessError(max(rcs), "nvcc -c")
+    link = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", LIB + ".tmp",
+            "-L", lib, f"-l:{libname}", "-Xlinker", f"-rpath,{lib}"]
+    print(" ".join(link), file=sys.stderr)
+    subprocess.check_call(link)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(tmp)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

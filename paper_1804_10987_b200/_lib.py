@@ -117,10 +117,15 @@ def dp_precode_mrt(ctx, H_ptr: int, s_ptr: int, N0: float, rho2: float, x_ptr: i
     return lib().dp_precode_mrt(ctx, H_ptr, s_ptr, float(N0), float(rho2), x_ptr, stream)
 
 
-def dp_set_clusters(ctx, B_c=None, power=None, tau=None) -> int:
-    """Sequences of C cluster sizes / power shares / tau values (None = the default)."""
+def dp_set_clusters(ctx, B_c=None, power=None, tau=None, C=None) -> int:
+    """Sequences of C cluster sizes / power shares / tau values (None = the default).  The C side
+    reads exactly C entries of each array, so when C is given every sequence must have length C."""
     def arr(ct, v):
-        return None if v is None else (ct * len(v))(*v)
+        if v is None:
+            return None
+        if C is not None and len(v) != C:
+            raise ValueError(f"dp_set_clusters: got {len(v)} entries, need C={C}")
+        return (ct * len(v))(*v)
     return lib().dp_set_clusters(ctx, arr(ctypes.c_int, B_c), arr(ctypes.c_double, power), arr(ctypes.c_double, tau))
 
 

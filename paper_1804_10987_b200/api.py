@@ -98,7 +98,7 @@ class Precoder:
         None = the default (equal split, 1/C, the constructor's tau).  include/dp.h dp_set_clusters."""
         L.check(L.dp_set_clusters(self.ctx, None if sizes is None else [int(v) for v in sizes],
                                   None if power is None else [float(v) for v in power],
-                                  None if tau is None else [float(v) for v in tau]), "dp_set_clusters")
+                                  None if tau is None else [float(v) for v in tau], C=self.C), "dp_set_clusters")
 
     # ------------------------------------------------------------ prepare / apply (P:286-289)
     def prepare_pd(self, H, N0: float, rho2: float = 1.0, stream=None):

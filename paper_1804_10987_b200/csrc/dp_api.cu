@@ -5,31 +5,9 @@
 // exchange steps (PD: Gram reduction P:280-281 and, in the paper's topology,
 // z broadcast P:296; FD: s broadcast P:255/P:299 and a 2*n_sc scalar
 // allreduce), host-pointer staging and kernel-level profiling.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-#include <cuda_runtime.h>
-#include <nccl.h>
+#include "dp_internal.cuh"
 
-#include <cmath>
-#include <cstdarg>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <string>
-#include <mutex>
-#include <unordered_map>
-#include <vector>
-
-#include "dp.h"
-#include "kernels.cuh"
-#include "fd_tc.cuh"
-#include "solve_mw.cuh"
-#include "precode_tc2.cuh"
-#include "gram_tc2.cuh"
-#include "ber.cuh"
-#include "fd_small.cuh"
-
-namespace {
+namespace dpi {
 
 thread_local std::string g_err;
 
@@ -42,178 +20,13 @@ int fail(int code, const char *fmt, ...) {
   g_err = buf;
   return code;
 }
+void clear_error() { g_err.clear(); }
 
-#define CK(call)                                                                                  \
-  do {                                                                                            \
-    cudaError_t e_ = (call);                                                                      \
-    if (e_ != cudaSuccess) return fail(DP_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,   \
-                                       cudaGetErrorString(e_));                                   \
-  } while (0)
-#define NK(call)                                                                                  \
-  do {                                                                                            \
-    ncclResult_t r_ = (call);                                                                     \
-    if (r_ != ncclSuccess) return fail(DP_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,   \
-                                       ncclGetErrorString(r_));                                   \
-  } while (0)
-#define RET(call)                 \
-  do {                            \
-    int rc_ = (call);             \
-    if (rc_ != DP_OK) return rc_; \
-  } while (0)
+}  // namespace dpi
 
-// count a collective's payload (floats) in the context's exchange ledger
-#define LEDGER(c, kind, nfloats) ((c)->ledger[(kind)] += (long long)(nfloats))
-
-struct ProfRec {
-  int kid;
-  cudaEvent_t a, b;
-};
-
-}  // namespace
-
-struct dp_ctx {
-  dp_config cfg;
-  int Bl = 0;        // antennas on this rank
-  int Cl = 0;        // clusters on this rank
-  int S = 0;         // cluster size B / C
-  int pd_chunk = 0;  // rows per SG chunk in the per-subcarrier PD kernels
-  int pd_nchunks = 0;
-  int pd_nw = 0;     // warps per CTA of the per-subcarrier PD kernels
-  int fd_nw = 0;     // warps per CTA of the FD fused kernel
-  int fdu_nw = 0;    // warps of the FD unfused per-subcarrier kernels (chunk = cluster)
-  bool comm_on = false;
-  bool use_tc = true;        // tensor-core paths where available (env DP_NO_TC=1 disables)
-  int num_sms = 148;
-  ncclComm_t comm = nullptr;
-  // device workspace
-  float2 *s_buf = nullptr;   // broadcast landing buffer for s
-  float2 *G = nullptr;       // packed Grams
-  float2 *z = nullptr;       // whitened symbols (unfused / T1)
-  float *beta = nullptr;     // per problem beta
-  float *pw = nullptr;       // power partials
-  float *fin = nullptr;      // [n_sc][2] per-subcarrier scalars
-  int *bad = nullptr;        // non-HPD counter
-  size_t pw_len = 0;
-  // host staging (host-pointer calls)
-  float2 *h_dev = nullptr, *s_dev = nullptr, *x_dev = nullptr;
-  cudaStream_t st_h2d = nullptr, st_d2h = nullptr;   // host-pointer pipeline copy streams
-  // host-side caches (per-frame host overhead): tensor maps by (pointer, rows, box, swizzle),
-  // device-ness of recently seen pointers
-  struct TmapEntry { const void *p; int rows, box, sw; CUtensorMap tm; };
-  std::vector<TmapEntry> tmaps;
-  std::vector<std::pair<const void *, bool>> ptr_kind;
-  // unequal clusters (dp_set_clusters; Eq. 9): this rank's clusters as maximal
-  // runs of equal (size, power share, tau); empty = the equal split B/C, rho^2/C, cfg.tau
-  struct VarRun { int cl0, len, S, off; double w, tau; };
-  std::vector<VarRun> vruns;
-  std::vector<int> vsizes;   // all C cluster sizes (global) when set
-  cudaStream_t st_run[3] = {nullptr, nullptr, nullptr};   // concurrent runs (fork / join on events)
-  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
-  // last call
-  int last_mode = -1;        // 0 pd, 1 fd
-  int prepared = -1;         // W cached in G by dp_prepare_pd (0) / dp_prepare_fd (1); -1 none
-  // profiling
-  std::vector<ProfRec> prof;
-  std::vector<cudaEvent_t> ev_pool;
-  double prof_ms[DP_NUM_KERNELS] = {0};
-  long long prof_n[DP_NUM_KERNELS] = {0};
-  long long launches = 0;
-  // exchange ledger: float payload elements handed to each kind of collective by this rank
-  long long ledger[DP_NUM_COMM] = {0};
-};
+using namespace dpi;
 
 namespace {
-
-int next_pow2(int v) {
-  int p = 1;
-  while (p < v) p <<= 1;
-  return p;
-}
-
-// precode/whitening symbol chunk KC: one chunk for K <= 16 (7, 8, 14 or 16), else chunks of 16
-int kc_of(int K) { return K == 7 ? 7 : K == 14 ? 14 : K <= 8 ? 8 : 16; }
-
-template <int KC>
-int zs_of(int K) { return dpk::ZL<KC>::zs(K); }
-int zs_rt(int K) {
-  switch (kc_of(K)) {
-    case 7: return zs_of<7>(K);
-    case 8: return zs_of<8>(K);
-    case 14: return zs_of<14>(K);
-    default: return zs_of<16>(K);
-  }
-}
-template <int U>
-int fd_scr_rt(int K) {
-  switch (kc_of(K)) {
-    case 7: return dpk::fd_scr_size<U, 7>(K);
-    case 8: return dpk::fd_scr_size<U, 8>(K);
-    case 14: return dpk::fd_scr_size<U, 14>(K);
-    default: return dpk::fd_scr_size<U, 16>(K);
-  }
-}
-template <int U>
-int solve_scr_rt(int K) {
-  switch (kc_of(K)) {
-    case 7: return dpk::solve_scr_size<U, 7>(K);
-    case 8: return dpk::solve_scr_size<U, 8>(K);
-    case 14: return dpk::solve_scr_size<U, 14>(K);
-    default: return dpk::solve_scr_size<U, 16>(K);
-  }
-}
-int fd_scr_u(int U, int K) {
-  return U == 4 ? fd_scr_rt<4>(K) : U == 8 ? fd_scr_rt<8>(K) : U == 16 ? fd_scr_rt<16>(K) : fd_scr_rt<32>(K);
-}
-int solve_scr_u(int U, int K) {
-  return U == 4 ? solve_scr_rt<4>(K) : U == 8 ? solve_scr_rt<8>(K) : U == 16 ? solve_scr_rt<16>(K)
-                                                                             : solve_scr_rt<32>(K);
-}
-
-// ---------------------------------------------------------------- smem sizes (bytes)
-size_t smem_fd_fused(int U, int S, int K, int nw) {
-  const int PPW = 32 / U;
-  return (size_t)nw * PPW * (S * U + fd_scr_u(U, K)) * sizeof(float2);
-}
-size_t smem_gram(int U, int Bl, int nw) {
-  return ((size_t)Bl * U + (size_t)(nw / 2) * 32 * (U / 2 + U / 4)) * sizeof(float2);
-}
-size_t smem_solve(int U, int K) { return (size_t)4 * (32 / U) * solve_scr_u(U, K) * sizeof(float2); }
-size_t smem_precode(int U, int Bl, int K, int zgroups) {
-  return ((size_t)Bl * U + (size_t)zgroups * U * zs_rt(K)) * sizeof(float2);
-}
-
-// ---------------------------------------------------------------- profiling helpers
-cudaEvent_t take_event(dp_ctx *c) {
-  if (!c->ev_pool.empty()) {
-    cudaEvent_t e = c->ev_pool.back();
-    c->ev_pool.pop_back();
-    return e;
-  }
-  cudaEvent_t e;
-  cudaEventCreate(&e);
-  return e;
-}
-
-struct LaunchScope {
-  dp_ctx *c;
-  int kid;
-  cudaStream_t st;
-  cudaEvent_t a = nullptr, b = nullptr;
-  LaunchScope(dp_ctx *c_, int kid_, cudaStream_t st_) : c(c_), kid(kid_), st(st_) {
-    c->launches++;
-    if (c->cfg.flags & DP_FLAG_PROFILE) {
-      a = take_event(c);
-      b = take_event(c);
-      cudaEventRecord(a, st);
-    }
-  }
-  ~LaunchScope() {
-    if (a) {
-      cudaEventRecord(b, st);
-      c->prof.push_back({kid, a, b});
-    }
-  }
-};
 
 int drain_profile(dp_ctx *c) {
   for (auto &r : c->prof) {
@@ -228,351 +41,6 @@ int drain_profile(dp_ctx *c) {
   c->prof.clear();
   return DP_OK;
 }
-
-// ---------------------------------------------------------------- kernel launchers
-using dpk::Args;
-
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size (host overhead
-// per frame matters when a rank's share of the frame is small, e.g. 8 GPUs)
-template <typename Kern>
-cudaError_t set_smem(Kern kern, size_t bytes) {
-  static std::mutex mu;
-  static std::unordered_map<const void *, size_t> done;
-  std::lock_guard<std::mutex> g(mu);
-  auto it = done.find((const void *)kern);
-  if (it != done.end() && it->second >= bytes) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) done[(const void *)kern] = bytes;
-  return e;
-}
-
-// Launch with programmatic dependent launch (PDL): the kernel may be scheduled while
-// its predecessor on the stream drains; every kernel starts with griddepcontrol.wait.
-template <typename Kern, typename... KArgs>
-cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const KArgs &...args) {
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  static const bool use_pdl = getenv("DP_NO_PDL") == nullptr;
-  cfg.attrs = attr;
-  cfg.numAttrs = use_pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, args...);
-}
-
-// PDL launch with a thread-block cluster shape (cluster_x CTAs along x)
-template <typename Kern, typename... KArgs>
-cudaError_t launch_pdl_cluster(Kern kern, dim3 grid, dim3 block, size_t smem, int cluster_x, cudaStream_t st,
-                               const KArgs &...args) {
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = cluster_x;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  static const bool use_pdl = getenv("DP_NO_PDL") == nullptr;
-  cfg.attrs = use_pdl ? attr : attr + 1;
-  cfg.numAttrs = use_pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...);
-}
-
-// FD small-cluster branch B_c = S < U (fd_small.cuh)
-template <int S, int U, int KC>
-int launch_fd_small_t(dp_ctx *c, const Args &a, cudaStream_t st) {
-  constexpr int NSG = 4 * (32 / S);                      // 4 warps per CTA
-  const size_t sm = (size_t)NSG * dpk::fds_size<S, U, KC>(a.K) * sizeof(float2);
-  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "FD small-cluster tiles need %zu B of shared memory", sm);
-  auto kern = dpk::fd_small_kernel<S, U, KC>;
-  CK(set_smem(kern, sm));
-  const int nprob = a.n_sc * a.nchunks;
-  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
-  CK(launch_pdl(kern, dim3((nprob + NSG - 1) / NSG), dim3(128), sm, st, a));
-  return DP_OK;
-}
-template <int S, int U>
-int launch_fd_small_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
-  switch (kc_of(a.K)) {
-    case 7: return launch_fd_small_t<S, U, 7>(c, a, st);
-    case 8: return launch_fd_small_t<S, U, 8>(c, a, st);
-    case 14: return launch_fd_small_t<S, U, 14>(c, a, st);
-    default: return launch_fd_small_t<S, U, 16>(c, a, st);
-  }
-}
-int launch_fd_small(dp_ctx *c, const Args &a, cudaStream_t st) {
-  const int S = a.S, U = c->cfg.U;
-  if (S == 4 && U == 8) return launch_fd_small_kc<4, 8>(c, a, st);
-  if (S == 4 && U == 16) return launch_fd_small_kc<4, 16>(c, a, st);
-  if (S == 4 && U == 32) return launch_fd_small_kc<4, 32>(c, a, st);
-  if (S == 8 && U == 16) return launch_fd_small_kc<8, 16>(c, a, st);
-  if (S == 8 && U == 32) return launch_fd_small_kc<8, 32>(c, a, st);
-  if (S == 16 && U == 32) return launch_fd_small_kc<16, 32>(c, a, st);
-  return fail(DP_ERR_UNSUPPORTED, "FD small-cluster branch: B_c=%d, U=%d (need B_c in {4, 8, 16} < U)", S, U);
-}
-
-template <int U, int KC>
-int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
-  const int nw = c->fd_nw;
-  const int nsg = nw * (32 / U);
-  const int nprob = a.n_sc * a.nchunks;
-  static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
-  const size_t sm = smem_fd_fused(U, a.S, a.K, nw) + pad;
-  auto kern = dpk::fd_fused_kernel<U, KC>;
-  CK(set_smem(kern, sm));
-  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
-  CK(launch_pdl(kern, dim3((nprob + nsg - 1) / nsg), dim3(nw * 32), sm, st, a));
-  return DP_OK;
-}
-
-int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw,
-                int U = 32);
-
-template <int CH, int U>
-int launch_gram_tc2(dp_ctx *c, const Args &b, cudaStream_t st) {
-  using T = dpk::GT2<CH, U>;
-  CUtensorMap tm;
-  RET(make_h_tmap(c, b.H, b.n_sc * b.Bl, &tm, CH, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, U));
-  auto kern = dpk::gram_tc2_kernel<CH, U>;
-  CK(set_smem(kern, T::SMEM));
-  LaunchScope ls(c, DP_KERNEL_GRAM, st);
-  CK(launch_pdl(kern, dim3(std::min(b.n_sc * b.nchunks, c->num_sms)), dim3(T::THREADS), T::SMEM, st, tm, b));
-  return DP_OK;
-}
-
-template <int U, bool PER_CHUNK>
-int launch_gram(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
-  if constexpr (U == 32 || U == 16) {
-    Args b = a;                                   // work item = (subcarrier, group)
-    if (!PER_CHUNK) {
-      b.S = a.Bl;                                 // one group: all local antennas
-      b.nchunks = 1;
-    }
-    // tensor-core Gram, operands straight from TMA.  U = 16 (M = 64 UMMAs) is correct but measured
-    // no faster than the SIMT kernel at cfg3 (17.3 vs 15.5 us: 128-antenna items are too small to
-    // amortise the per-item epilogue), so it is opt-in (DP_GRAM_TC16)
-    static const bool tc16 = getenv("DP_GRAM_TC16") != nullptr;
-    if (c->use_tc && b.S % 32 == 0 && (U == 32 || tc16))
-      return (b.S % 64 == 0) ? launch_gram_tc2<64, U>(c, b, st) : launch_gram_tc2<32, U>(c, b, st);
-  }
-  const size_t sm = smem_gram(U, a.Bl, nw);
-  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "Gram tile needs %zu B of shared memory", sm);
-  auto kern = dpk::gram_kernel<U, PER_CHUNK>;
-  CK(set_smem(kern, sm));
-  LaunchScope ls(c, DP_KERNEL_GRAM, st);
-  CK(launch_pdl(kern, dim3(a.n_sc), dim3(nw * 32), sm, st, a));
-  return DP_OK;
-}
-
-template <int U, int KC>
-int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
-  const int nprob = a.n_sc * a.groups;
-  if constexpr (U == 32) {
-    static const bool sg_only = getenv("DP_SOLVE_SG") != nullptr;   // A/B: one warp per problem
-    static const int nw_env = getenv("DP_SOLVE_NW") ? atoi(getenv("DP_SOLVE_NW")) : 4;
-    if (!sg_only) {                                                  // 4 (or 2) warps per problem (solve_mw.cuh)
-      const int NW = nw_env == 2 ? 2 : 4;
-      // whitening in symbol chunks of at most 8: at 9 CTAs / SM (56 registers) 14 or 16
-      // accumulators spilled
-      constexpr int KS = KC > 8 ? KC / 2 : KC;
-      const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KS, NW) * sizeof(float2);
-      auto kern = NW == 4 ? dpk::solve_mw_kernel<KS, 4> : dpk::solve_mw_kernel<KS, 2>;
-      CK(set_smem(kern, sm));
-      LaunchScope ls(c, DP_KERNEL_SOLVE, st);
-      CK(launch_pdl(kern, dim3((nprob + 4 / NW - 1) / (4 / NW)), dim3(dpk::SMW_THREADS), sm, st, a));
-      return DP_OK;
-    }
-  }
-  // few problems (PD: one per subcarrier): one warp per CTA spreads the ~9k-instruction
-  // warps evenly over the SMs (4-warp CTAs left some SMs with 50% more work)
-  const int wpc = (nprob / (32 / U) <= 16 * c->num_sms) ? 1 : 4;
-  const int per = wpc * (32 / U);
-  const size_t sm = smem_solve(U, a.K) / 4 * wpc;
-  auto kern = dpk::solve_kernel<U, KC>;
-  CK(set_smem(kern, sm));
-  LaunchScope ls(c, DP_KERNEL_SOLVE, st);
-  CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(32 * wpc), sm, st, a));
-  return DP_OK;
-}
-
-template <int U, int KC>
-int launch_precode(dp_ctx *c, const Args &a, int nw, cudaStream_t st) {
-  const size_t sm = smem_precode(U, a.Bl, a.K, a.zgroups);
-  if (sm > 227 * 1024) return fail(DP_ERR_UNSUPPORTED, "precode tile needs %zu B of shared memory", sm);
-  auto kern = dpk::precode_kernel<U, KC>;
-  CK(set_smem(kern, sm));
-  LaunchScope ls(c, DP_KERNEL_PRECODE, st);
-  CK(launch_pdl(kern, dim3(a.n_sc), dim3(nw * 32), sm, st, a));
-  return DP_OK;
-}
-
-// 2-D tensor map over H_local viewed as fp32 [n_sc * Bl][64] (U = 32), box_rows-row x
-// 32-float boxes, 128-byte swizzle (the canonical K-major SW128 UMMA layout).
-int encode_h_tmap(const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw, int U) {
-  static PFN_cuTensorMapEncodeTiled encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) != cudaSuccess ||
-        !encode)
-      return fail(DP_ERR_CUDA, "cuTensorMapEncodeTiled not available");
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)(2 * U), (cuuint64_t)rows};   // fp32 [rows][2U]
-  cuuint64_t strides[1] = {(cuuint64_t)(2 * U * 4)};
-  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)H, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(DP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return DP_OK;
-}
-
-int make_h_tmap(dp_ctx *c, const float2 *H, int rows, CUtensorMap *tm, int box_rows, CUtensorMapSwizzle sw, int U) {
-  const int key = (int)sw + 16 * U;
-  for (const auto &e : c->tmaps)
-    if (e.p == H && e.rows == rows && e.box == box_rows && e.sw == key) {
-      *tm = e.tm;
-      return DP_OK;
-    }
-  RET(encode_h_tmap(H, rows, tm, box_rows, sw, U));
-  if (c->tmaps.size() >= 16) c->tmaps.erase(c->tmaps.begin());
-  c->tmaps.push_back({H, rows, box_rows, key, *tm});
-  return DP_OK;
-}
-
-// PD precode on the tensor cores (precode_tc2.cuh): U = 32, one z per subcarrier,
-// K <= 16, 128-antenna blocks
-bool precode_tc2_ok(const dp_ctx *c, const Args &a) {
-  static const bool off = getenv("DP_NO_PC2") != nullptr;
-  return !off && c->use_tc && c->cfg.U == 32 && a.K <= 16 && a.Bl % dpk::PC2_ROWS == 0 && a.zgroups == 1;
-}
-
-int launch_precode_tc2(dp_ctx *c, const Args &a, cudaStream_t st) {
-  CUtensorMap tm;
-  RET(make_h_tmap(c, a.H, a.n_sc * a.Bl, &tm, dpk::PC2_ROWS, CU_TENSOR_MAP_SWIZZLE_128B));
-  auto kern = dpk::precode_tc2_kernel;
-  CK(set_smem(kern, dpk::PC2_SMEM));
-  LaunchScope ls(c, DP_KERNEL_PRECODE, st);
-  CK(launch_pdl(kern, dim3(std::min(a.n_sc, c->num_sms)), dim3(dpk::PC2_THREADS), dpk::PC2_SMEM, st, tm, a));
-  return DP_OK;
-}
-
-// FD with the cluster Gram on the tensor cores: U = 32, S = 32 (fd_tc.cuh)
-bool fd_tc_ok(const dp_ctx *c, const Args &a) {
-  static const bool off = getenv("DP_NO_TC_FD") != nullptr;
-  return !off && c->use_tc && c->cfg.U == 32 && a.S == 32 && a.K <= 16;
-}
-
-// fd_tc folds the per-subcarrier scalars into the kernel (no fd_finish_kernel) when the
-// rank's clusters of a subcarrier fill whole CTAs (Cl = 4, 8, 16, 32: a cluster of Cl/4
-// CTAs) or a CTA holds whole subcarriers (Cl = 1, 2, 4).  Returns CTAs per subcarrier, 0 = off.
-int fd_fold_of(const dp_ctx *c, const Args &a) {
-  static const bool off = getenv("DP_NO_FOLD") != nullptr;
-  if (off || a.Gout || !c->vruns.empty()) return 0;
-  const int Cl = a.nchunks;
-  if (Cl == 4 || Cl == 8 || Cl == 16 || Cl == 32) return Cl / 4;
-  if (4 % Cl == 0) return 1;
-  return 0;
-}
-
-template <int KC, bool WTC>
-int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
-  CUtensorMap tm;
-  RET(make_h_tmap(c, a.H, a.n_sc * a.Bl - a.hrow_off, &tm, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
-  auto kern = dpk::fd_tc_kernel<KC, WTC>;
-  static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
-  const size_t smem = dpk::FDT_SMEM + pad;
-  CK(set_smem(kern, smem));
-  const int nprob = a.n_sc * a.nchunks;
-  Args b = a;
-  // resident CTAs: 3 per SM; the L2 prefetch assumes contiguous clusters (off for unequal runs)
-  b.pf_dist = a.Bl == a.nchunks * 32 ? 3 * c->num_sms : 0;
-  b.fold = fd_fold_of(c, a);
-  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
-  if (b.fold > 1)
-    CK(launch_pdl_cluster(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), smem, b.fold, st, tm, b));
-  else
-    CK(launch_pdl(kern, dim3((nprob + 3) / 4), dim3(dpk::FDT_THREADS), smem, st, tm, b));
-  return DP_OK;
-}
-int launch_fd_tc_kc(dp_ctx *c, const Args &a, cudaStream_t st) {
-  static const bool simt_w = getenv("DP_FD_SIMT_WHITEN") != nullptr;   // A/B: SIMT whitening
-  // tensor-core whitening stacks a CTA's 4 problems on one s: they must share the subcarrier
-  if (simt_w || a.nchunks % 4 != 0) {
-    switch (kc_of(a.K)) {
-      case 7: return launch_fd_tc<7, false>(c, a, st);
-      case 8: return launch_fd_tc<8, false>(c, a, st);
-      case 14: return launch_fd_tc<14, false>(c, a, st);
-      default: return launch_fd_tc<16, false>(c, a, st);
-    }
-  }
-  switch (kc_of(a.K)) {
-    case 7: return launch_fd_tc<7, true>(c, a, st);
-    case 8: return launch_fd_tc<8, true>(c, a, st);
-    case 14: return launch_fd_tc<14, true>(c, a, st);
-    default: return launch_fd_tc<16, true>(c, a, st);
-  }
-}
-
-
-// ---------------------------------------------------------------- U / KC dispatch
-template <template <int, int> class F, int U, typename... T>
-int dispatch_kc(int K, T... args) {
-  switch (kc_of(K)) {
-    case 7: return F<U, 7>::run(args...);
-    case 8: return F<U, 8>::run(args...);
-    case 14: return F<U, 14>::run(args...);
-    default: return F<U, 16>::run(args...);
-  }
-}
-template <template <int, int> class F, typename... T>
-int dispatch(int U, int K, T... args) {
-  switch (U) {
-    case 4: return dispatch_kc<F, 4>(K, args...);
-    case 8: return dispatch_kc<F, 8>(K, args...);
-    case 16: return dispatch_kc<F, 16>(K, args...);
-    case 32: return dispatch_kc<F, 32>(K, args...);
-  }
-  return fail(DP_ERR_UNSUPPORTED, "U=%d: kernels are instantiated for U in {4, 8, 16, 32}", U);
-}
-
-template <int U, int KC> struct FdFused {
-  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_fd_fused<U, KC>(c, a, st); }
-};
-template <int U, int KC> struct GramSum {
-  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) { return launch_gram<U, false>(c, a, nw, st); }
-};
-template <int U, int KC> struct GramPer {
-  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) { return launch_gram<U, true>(c, a, nw, st); }
-};
-template <int U, int KC> struct Precode {
-  static int run(dp_ctx *c, Args a, int nw, cudaStream_t st) { return launch_precode<U, KC>(c, a, nw, st); }
-};
-template <int U, int KC>
-int launch_whiten(dp_ctx *c, const Args &a, cudaStream_t st) {
-  const int nprob = a.n_sc * a.groups;
-  const int per = 4 * (32 / U);
-  const size_t sm = (size_t)per * (dpk::npacked(U) + a.K * U + U * dpk::ZL<KC>::zs(a.K)) * sizeof(float2);
-  auto kern = dpk::whiten_kernel<U, KC>;
-  CK(set_smem(kern, sm));
-  LaunchScope ls(c, DP_KERNEL_SOLVE, st);
-  CK(launch_pdl(kern, dim3((nprob + per - 1) / per), dim3(128), sm, st, a));
-  return DP_OK;
-}
-template <int U, int KC> struct Whiten {
-  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_whiten<U, KC>(c, a, st); }
-};
-template <int U, int KC> struct Solve {
-  static int run(dp_ctx *c, Args a, cudaStream_t st) { return launch_solve<U, KC>(c, a, st); }
-};
 
 // ---------------------------------------------------------------- helpers
 int alloc(void **p, size_t bytes) {
@@ -699,7 +167,6 @@ int finish_call(dp_ctx *c, bool host, dp_c32 *x, cudaStream_t st) {
 // -- the same kernels as the equal split, H / x offset to the run's first antenna with the
 // rank's row stride Bl -- into per-run beta / power scratch, then fd_var_finish_kernel
 // (beta_c in [sc][Cl] order, fin = {sum_c 1/beta_c, sum_c power_c}).  mrt: the MRT precoder.
-int launch_mrt_u(dp_ctx *c, const Args &a, cudaStream_t st);
 // FD / MRT need cluster sizes: the equal split, or dp_set_clusters when C does not divide B
 int need_split(const dp_ctx *c) {
   if (c->S == 0 && c->vruns.empty())
@@ -711,30 +178,22 @@ int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, dou
                 cudaStream_t st) {
   const dp_config &k = c->cfg;
   const size_t n = (size_t)k.n_sc * c->Cl;
-  float *vb = nullptr;
-  CK(cudaMallocAsync((void **)&vb, 2 * n * sizeof(float), st));
+  float *vb = c->vb;                                      // allocated by dp_set_clusters (no allocation here)
   dpk::VarRuns vr;
   memset(&vr, 0, sizeof(vr));
   vr.n = (int)c->vruns.size();
   vr.Cl = c->Cl;
   vr.vb = vb;
   vr.vp = vb + n;
-  int rc = DP_OK;
-  // the runs touch disjoint H rows, x columns and scratch: up to 3 run on their own streams so
-  // their partial waves overlap (fork after the scratch allocation, join before the finish)
+  // the runs touch disjoint H rows, x columns and scratch: up to 3 run on the context's own streams
+  // (created by dp_set_clusters) so their partial waves overlap; fork on an event, join before the finish
   static const bool serial = getenv("DP_VAR_SERIAL") != nullptr;
-  const int nfork = serial ? 0 : std::min(vr.n, 3);
+  const int nfork = (serial || !c->run_streams) ? 0 : std::min(vr.n, 3);
   if (nfork > 1) {
-    if (!c->ev_fork) {
-      CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-      for (int j = 0; j < 3; ++j) {
-        CK(cudaStreamCreateWithFlags(&c->st_run[j], cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&c->ev_join[j], cudaEventDisableTiming));
-      }
-    }
     CK(cudaEventRecord(c->ev_fork, st));
     for (int j = 0; j < nfork; ++j) CK(cudaStreamWaitEvent(c->st_run[j], c->ev_fork, 0));
   }
+  int rc = DP_OK;
   for (int i = 0; i < vr.n && rc == DP_OK; ++i) {
     const cudaStream_t sr = nfork > 1 ? c->st_run[i % nfork] : st;
     const auto &r = c->vruns[i];
@@ -757,20 +216,15 @@ int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, dou
     if (mrt) rc = launch_mrt_u(c, a, sr);
     else if (r.S < k.U) rc = launch_fd_small(c, a, sr);
     else if (fd_tc_ok(c, a)) rc = launch_fd_tc_kc(c, a, sr);
-    else rc = dispatch<FdFused>(k.U, k.K, c, a, sr);
+    else rc = launch_fd_fused_any(c, a, sr);
   }
-  if (nfork > 1)
+  if (nfork > 1)                                          // join even after a failed launch
     for (int j = 0; j < nfork; ++j) {
-      CK(cudaEventRecord(c->ev_join[j], c->st_run[j]));
-      CK(cudaStreamWaitEvent(st, c->ev_join[j], 0));
+      const cudaError_t e1 = cudaEventRecord(c->ev_join[j], c->st_run[j]);
+      const cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(st, c->ev_join[j], 0) : e1;
+      if (e2 != cudaSuccess && rc == DP_OK) rc = fail(DP_ERR_CUDA, "fork/join: %s", cudaGetErrorString(e2));
     }
-  if (rc == DP_OK) {
-    Args a = base_args(c);
-    LaunchScope ls(c, DP_KERNEL_FINISH, st);
-    const cudaError_t e = launch_pdl(dpk::fd_var_finish_kernel, dim3((k.n_sc + 3) / 4), dim3(128), 0, st, a, vr);
-    if (e != cudaSuccess) rc = fail(DP_ERR_CUDA, "fd_var_finish_kernel: %s", cudaGetErrorString(e));
-  }
-  CK(cudaFreeAsync(vb, st));
+  if (rc == DP_OK) rc = launch_fd_var_finish(c, base_args(c), vr, st);
   return rc;
 }
 
@@ -797,20 +251,19 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   } else if (c->S < k.U) {
     // small clusters (B_c < U): B_c x B_c regularised Gram per cluster
     RET(launch_fd_small(c, a, st));
-    LaunchScope ls(c, DP_KERNEL_FINISH, st);
-    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+    RET(launch_fd_finish(c, a, st));
   } else if (k.flags & DP_FLAG_UNFUSED) {
     // (a) per-cluster Grams -> (b) solve+whiten per cluster -> (c) precode
     a.Gout = c->G;
-    RET(dispatch<GramPer>(k.U, k.K, c, a, c->fdu_nw, st));
+    RET(launch_gram_any(c, a, c->fdu_nw, true, st));
     a.G = c->G;
     a.groups = c->Cl;
     a.zout = c->z;
-    RET(dispatch<Solve>(k.U, k.K, c, a, st));
+    RET(launch_solve_any(c, a, st));
     a.zin = c->z;
     a.zgroups = c->Cl;
     a.chunks_per_zgroup = 1;
-    RET(dispatch<Precode>(k.U, k.K, c, a, c->fdu_nw, st));
+    RET(launch_precode_any(c, a, c->fdu_nw, st));
   } else {
     const bool tc = fd_tc_ok(c, a);
     // SIMT kernel: fold the scalars when every CTA holds whole subcarriers
@@ -819,13 +272,11 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
     if (tc) RET(launch_fd_tc_kc(c, a, st));
     else {
       a.fold = simt_fold ? 1 : 0;
-      RET(dispatch<FdFused>(k.U, k.K, c, a, st));
+      RET(launch_fd_fused_any(c, a, st));
       a.fold = 0;
     }
-    if ((tc && fd_fold_of(c, a) == 0) || (!tc && !simt_fold)) {   // scalars not folded into the kernel
-      LaunchScope ls(c, DP_KERNEL_FINISH, st);
-      CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
-    }
+    if ((tc && fd_fold_of(c, a) == 0) || (!tc && !simt_fold))   // scalars not folded into the kernel
+      RET(launch_fd_finish(c, a, st));
   }
   if (c->comm_on) {
     NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
@@ -837,23 +288,6 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
 }
 
 // Fully-distributed MRT frame (Fig. 2 baseline) on device pointers
-template <int U>
-int launch_mrt(dp_ctx *c, const Args &a, cudaStream_t st) {
-  const size_t sm = (size_t)4 * a.K * U * sizeof(float2);
-  auto kern = dpk::mrt_kernel<U>;
-  CK(set_smem(kern, sm));
-  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
-  CK(launch_pdl(kern, dim3((a.n_sc * a.nchunks + 3) / 4), dim3(128), sm, st, a));
-  return DP_OK;
-}
-int launch_mrt_u(dp_ctx *c, const Args &a, cudaStream_t st) {
-  switch (c->cfg.U) {
-    case 4: return launch_mrt<4>(c, a, st);
-    case 8: return launch_mrt<8>(c, a, st);
-    case 16: return launch_mrt<16>(c, a, st);
-    default: return launch_mrt<32>(c, a, st);
-  }
-}
 int precode_mrt_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, double rho2, float2 *xd,
                     cudaStream_t st) {
   (void)N0;                                               // MRT ignores the noise level
@@ -873,8 +307,7 @@ int precode_mrt_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, do
     RET(fd_var_runs(c, Hd, s_use, 0.0, rho2, xd, true, st));
   } else {
     RET(launch_mrt_u(c, a, st));
-    LaunchScope ls(c, DP_KERNEL_FINISH, st);
-    CK(launch_pdl(dpk::fd_finish_kernel, dim3((k.n_sc + 127) / 128), dim3(128), 0, st, a));
+    RET(launch_fd_finish(c, a, st));
   }
   if (c->comm_on) {
     NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
@@ -908,7 +341,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   // (a) Gram of this rank's antennas: first levels of the adder tree G = sum_c G_c
   const size_t nG = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
   a.Gout = c->G;
-  RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));
+  RET(launch_gram_any(c, a, c->pd_nw, false, st));
   a.G = c->G;
   a.zout = c->z;
   if (topo_t3) {
@@ -925,7 +358,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
     b.s = s_use + (size_t)sc0 * k.K * k.U;
     b.zout = c->z + (size_t)sc0 * k.K * k.U;
     b.beta = c->beta + sc0;
-    RET(dispatch<Solve>(k.U, k.K, c, b, st));
+    RET(launch_solve_any(c, b, st));
     NK(ncclGroupStart());
     NK(ncclAllGather(c->z + (size_t)sc0 * k.K * k.U, c->z, blkZ, ncclFloat, c->comm, st));
     NK(ncclAllGather(c->beta + sc0, c->beta, (size_t)nb, ncclFloat, c->comm, st));
@@ -941,7 +374,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
     LEDGER(c, DP_COMM_GRAM, nG);
   }
   // (b) whitening node: A = G + kappa I, LDL^H, A^{-1}, beta (Lemma 1), z = A^{-1} s / beta
-  if (!topo_t3 && (!topo_t1 || k.rank == 0)) RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  if (!topo_t3 && (!topo_t1 || k.rank == 0)) RET(launch_solve_any(c, a, st));
   if (topo_t1) {
     // master broadcasts z and beta
     NK(ncclGroupStart());
@@ -957,7 +390,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   if (precode_tc2_ok(c, a)) {
     RET(launch_precode_tc2(c, a, st));               // tensor-core precode, writes the scalars
   } else {
-    RET(dispatch<Precode>(k.U, k.K, c, a, c->pd_nw, st));
+    RET(launch_precode_any(c, a, c->pd_nw, st));
   }
   // per-subcarrier scalars (written by the precode kernel): power summed over ranks
   if (c->comm_on) {
@@ -1139,6 +572,7 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   A((void **)&c->pw, c->pw_len * 4);
   A((void **)&c->fin, n_sc * 2 * 4);
   A((void **)&c->bad, 4);
+  A((void **)&c->rd_buf, n_sc * 4);
   if (rc != DP_OK) {
     std::string e = g_err;
     dp_finalize(c);
@@ -1181,18 +615,9 @@ int dp_read_scalars(dp_ctx *c, int which, float *dst, void *stream) {
     const size_t n = (size_t)n_sc * (c->last_mode == 1 ? c->Cl : 1);
     CK(cudaMemcpyAsync(dst, c->beta, n * 4, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   } else if (which == DP_SCALAR_RX || which == DP_SCALAR_POWER) {
-    float *d = dst;
-    float *tmp = nullptr;
-    if (!dev) {
-      CK(cudaMallocAsync((void **)&tmp, (size_t)n_sc * 4, st));
-      d = tmp;
-    }
-    dpk::read_scalars_kernel<<<(n_sc + 127) / 128, 128, 0, st>>>(c->fin, n_sc, which, d);
-    CK(cudaGetLastError());
-    if (!dev) {
-      CK(cudaMemcpyAsync(dst, tmp, (size_t)n_sc * 4, cudaMemcpyDeviceToHost, st));
-      CK(cudaFreeAsync(tmp, st));
-    }
+    float *d = dev ? dst : c->rd_buf;                     // host dst: through the context's staging buffer
+    RET(launch_read_scalars(c->fin, n_sc, which, d, st));
+    if (!dev) CK(cudaMemcpyAsync(dst, c->rd_buf, (size_t)n_sc * 4, cudaMemcpyDeviceToHost, st));
   } else {
     return fail(DP_ERR_INVALID, "unknown scalar %d", which);
   }
@@ -1296,6 +721,20 @@ int dp_set_clusters(dp_ctx *c, const int *B_c, const double *power, const double
   }
   if (!equal && (int)runs.size() > dpk::VAR_MAX_RUNS)
     return fail(DP_ERR_UNSUPPORTED, "%d runs of equal clusters > %d", (int)runs.size(), dpk::VAR_MAX_RUNS);
+  if (!equal) {
+    // run scratch and the fork/join streams are created here, once, so FD / MRT calls with
+    // unequal clusters allocate nothing (dp.h: no allocation in precode calls)
+    CK(cudaSetDevice(k.device));
+    if (!c->vb) RET(alloc((void **)&c->vb, 2 * (size_t)k.n_sc * c->Cl * sizeof(float)));
+    if (runs.size() > 1 && !c->run_streams) {
+      for (int j = 0; j < 3; ++j) {
+        if (!c->st_run[j]) CK(cudaStreamCreateWithFlags(&c->st_run[j], cudaStreamNonBlocking));
+        if (!c->ev_join[j]) CK(cudaEventCreateWithFlags(&c->ev_join[j], cudaEventDisableTiming));
+      }
+      if (!c->ev_fork) CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      c->run_streams = true;                              // only once every stream and event exists
+    }
+  }
   if (equal) {
     c->vruns.clear();
     c->vsizes.clear();
@@ -1321,7 +760,7 @@ int dp_finalize(dp_ctx *c) {
     if (c->ev_join[j]) cudaEventDestroy(c->ev_join[j]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev};
+  void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev, c->vb, c->rd_buf};
   for (void *b : bufs)
     if (b) cudaFree(b);
   delete c;
@@ -1342,11 +781,11 @@ int dp_debug_gram(dp_ctx *c, const dp_c32 *H, int per_cluster, dp_c32 *G, void *
     a.S = c->S;
     a.nchunks = c->Cl;
     if (fd_tc_ok(c, a)) RET(launch_fd_tc_kc(c, a, st));   // the FD path's own (tensor-core) Gram
-    else RET(dispatch<GramPer>(c->cfg.U, c->cfg.K, c, a, c->fdu_nw, st));
+    else RET(launch_gram_any(c, a, c->fdu_nw, true, st));
   } else {
     a.S = c->pd_chunk;
     a.nchunks = c->pd_nchunks;
-    RET(dispatch<GramSum>(c->cfg.U, c->cfg.K, c, a, c->pd_nw, st));
+    RET(launch_gram_any(c, a, c->pd_nw, false, st));
   }
   return DP_OK;
 }
@@ -1364,7 +803,7 @@ int dp_debug_solve(dp_ctx *c, const dp_c32 *G, int groups, const dp_c32 *s, doub
   a.beta = beta;
   a.kappa = (float)kappa;
   a.coef = (float)(c->cfg.Es / rho_x2);
-  RET(dispatch<Solve>(c->cfg.U, c->cfg.K, c, a, st));
+  RET(launch_solve_any(c, a, st));
   return DP_OK;
 }
 
@@ -1397,7 +836,7 @@ int prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G, double N0, double rho2
   a.G = c->G;
   a.Wout = c->G;
   a.s = nullptr;
-  RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  RET(launch_solve_any(c, a, st));
   c->prepared = fd;
   return DP_OK;
 }
@@ -1420,14 +859,15 @@ int dp_prepare_pd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
   a.groups = 1;
   a.nbeta = 1;
   a.Gout = c->G;
-  RET(dispatch<GramSum>(k.U, k.K, c, a, c->pd_nw, st));   // G_c summed over local clusters
-  if (c->comm_on)                                         // every rank holds sum_c G_c
+  RET(launch_gram_any(c, a, c->pd_nw, false, st));   // G_c summed over local clusters
+  if (c->comm_on) {                                       // every rank holds sum_c G_c
     NK(ncclAllReduce(c->G, c->G, (size_t)k.n_sc * dpk::npacked(k.U) * 2, ncclFloat, ncclSum, c->comm, st));
     LEDGER(c, DP_COMM_GRAM, (size_t)k.n_sc * dpk::npacked(k.U) * 2);
+  }
   a.G = c->G;
   a.Wout = c->G;                                          // W = A^{-1}/beta in place of G
   a.s = nullptr;
-  RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  RET(launch_solve_any(c, a, st));
   c->prepared = 0;
   return DP_OK;
 }
@@ -1454,12 +894,12 @@ int dp_prepare_fd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
   a.groups = c->Cl;
   a.nbeta = c->Cl;
   a.Gout = c->G;
-  RET(dispatch<GramPer>(k.U, k.K, c, a, c->fdu_nw, st));  // G_c per local cluster
+  RET(launch_gram_any(c, a, c->fdu_nw, true, st));  // G_c per local cluster
   a.Gout = nullptr;
   a.G = c->G;
   a.Wout = c->G;
   a.s = nullptr;
-  RET(dispatch<Solve>(k.U, k.K, c, a, st));
+  RET(launch_solve_any(c, a, st));
   c->prepared = 1;
   return DP_OK;
 }
@@ -1502,21 +942,21 @@ int dp_apply(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, int Ka, dp_c32 *x, voi
   a.groups = fd ? c->Cl : 1;
   a.nbeta = fd ? c->Cl : 1;
   a.fin_inv_beta = (fd || k.rank == 0) ? 1 : 0;
-  RET(dispatch<Whiten>(k.U, Ka, c, a, st));                // z = W s
+  RET(launch_whiten_any(c, a, st));                // z = W s
   a.zin = c->z;
   if (fd) {
     a.S = c->S;
     a.nchunks = c->Cl;
     a.zgroups = c->Cl;
     a.chunks_per_zgroup = 1;
-    RET(dispatch<Precode>(k.U, Ka, c, a, c->fdu_nw, st));  // x_c = H_c^H z_c
+    RET(launch_precode_any(c, a, c->fdu_nw, st));  // x_c = H_c^H z_c
   } else {
     a.S = c->pd_chunk;
     a.nchunks = c->pd_nchunks;
     a.zgroups = 1;
     a.chunks_per_zgroup = c->pd_nchunks;
     if (precode_tc2_ok(c, a)) RET(launch_precode_tc2(c, a, st));
-    else RET(dispatch<Precode>(k.U, Ka, c, a, c->pd_nw, st));
+    else RET(launch_precode_any(c, a, c->pd_nw, st));
   }
   if (c->comm_on) {
     NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
@@ -1532,68 +972,6 @@ int dp_apply(dp_ctx *c, const dp_c32 *H, const dp_c32 *s, int Ka, dp_c32 *x, voi
       return fail(DP_ERR_NUMERIC, "%d (subcarrier, cluster) problems had a non-HPD regularised Gram", nb);
     }
   }
-  return DP_OK;
-}
-
-// ---------------------------------------------------------------- BER harness (f1)
-namespace {
-int qam_of(int M, dpk::Qam *q) {
-  int hb = 0;
-  while ((1 << (2 * hb)) < M) ++hb;
-  if (M != 4 && M != 16 && M != 64 && M != 256) return fail(DP_ERR_INVALID, "M=%d: square QAM with M in {4,16,64,256}", M);
-  q->hb = hb;
-  q->m = 1 << hb;
-  q->scale = (float)std::sqrt(3.0 / (2.0 * (M - 1)));
-  return DP_OK;
-}
-int check_dims(int n_sc, int B, int U, int K) {
-  if (n_sc <= 0 || B <= 0 || U <= 0 || K <= 0 || U > 32 || B > 256 || K > 16)
-    return fail(DP_ERR_INVALID, "dims n_sc=%d B=%d U=%d K=%d (need > 0, U <= 32, B <= 256, K <= 16)", n_sc, B, U, K);
-  return DP_OK;
-}
-}  // namespace
-
-int dp_synth_frame(unsigned long long seed, unsigned long long frame, int n_sc, int B, int U, int K, int M, double N0,
-                   dp_c32 *H, dp_c32 *s, unsigned char *idx, dp_c32 *noise, void *stream) {
-  g_err.clear();
-  RET(check_dims(n_sc, B, U, K));
-  if (!H || !s || !idx) return fail(DP_ERR_INVALID, "H, s and idx must be device pointers");
-  if (!(N0 >= 0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
-  dpk::SynthArgs a;
-  RET(qam_of(M, &a.q));
-  a.seed = seed;
-  a.frame = (uint32_t)frame;
-  a.n_sc = n_sc; a.B = B; a.U = U; a.K = K;
-  a.sigma_n = (float)std::sqrt(N0 / 2.0);
-  a.H = reinterpret_cast<float2 *>(H);
-  a.s = reinterpret_cast<float2 *>(s);
-  a.noise = reinterpret_cast<float2 *>(noise);
-  a.idx = idx;
-  const size_t n = std::max((size_t)n_sc * B * U, (size_t)n_sc * K * U);
-  const size_t thr = (n + 1) / 2;
-  dpk::synth_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, (cudaStream_t)stream>>>(a);
-  CK(cudaGetLastError());
-  return DP_OK;
-}
-
-int dp_receive_count(int n_sc, int B, int U, int K, int M, const dp_c32 *H, const dp_c32 *x, const dp_c32 *noise,
-                     const float *rx, const unsigned char *idx, unsigned long long *errors, void *stream) {
-  g_err.clear();
-  RET(check_dims(n_sc, B, U, K));
-  if (!H || !x || !rx || !idx || !errors) return fail(DP_ERR_INVALID, "NULL argument");
-  dpk::RxArgs a;
-  RET(qam_of(M, &a.q));
-  a.n_sc = n_sc; a.B = B; a.U = U; a.K = K;
-  a.H = reinterpret_cast<const float2 *>(H);
-  a.x = reinterpret_cast<const float2 *>(x);
-  a.noise = reinterpret_cast<const float2 *>(noise);
-  a.rx = rx;
-  a.idx = idx;
-  a.errors = errors;
-  const size_t sm = ((size_t)B * U + (size_t)K * B) * sizeof(float2);
-  CK(set_smem(dpk::rx_count_kernel, sm));
-  dpk::rx_count_kernel<<<n_sc, 256, sm, (cudaStream_t)stream>>>(a);
-  CK(cudaGetLastError());
   return DP_OK;
 }
 

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
+
 namespace dpk {
 
 // ------------------------------------------------------------------ complex helpers
@@ -1143,7 +1145,7 @@ __global__ void __launch_bounds__(128) mrt_kernel(Args a) {
 // Per subcarrier, fixed order over the local clusters: fin[sc] = {sum_c 1/beta_c,
 // sum_c power_c}.  (A separate grid: folding it into the fused kernel needs a
 // release fence per cluster, which waits for that warp's x stores and cost ~10%.)
-__global__ void __launch_bounds__(128) fd_finish_kernel(Args a) {
+static __global__ void __launch_bounds__(128) fd_finish_kernel(Args a) {
   pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
                    // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
@@ -1162,7 +1164,7 @@ struct VarRuns {
   const float *vb, *vp;
   int cl0[VAR_MAX_RUNS], len[VAR_MAX_RUNS];
 };
-__global__ void __launch_bounds__(128) fd_var_finish_kernel(Args a, VarRuns r) {
+static __global__ void __launch_bounds__(128) fd_var_finish_kernel(Args a, VarRuns r) {
   pdl_trigger();
   pdl_wait();
   // one warp per subcarrier, lane = cluster (strided); butterfly sums in a fixed order
@@ -1190,7 +1192,7 @@ __global__ void __launch_bounds__(128) fd_var_finish_kernel(Args a, VarRuns r) {
 }
 
 // which: 1 -> rx = 1 / fin[.][0] ; 2 -> power = fin[.][1]
-__global__ void read_scalars_kernel(const float *fin, int n_sc, int which, float *dst) {
+static __global__ void read_scalars_kernel(const float *fin, int n_sc, int which, float *dst) {
   const int sc = blockIdx.x * blockDim.x + threadIdx.x;
   if (sc >= n_sc) return;
   dst[sc] = (which == 1) ? 1.f / fin[2 * sc] : fin[2 * sc + 1];

@@ -1,6 +1,8 @@
 // tc_probe.cu — experiment harness for the tcgen05 helpers (not part of libdp.so):
 // D[64][64] = A[64][K] * B[64][K]^T with kind::tf32 UMMA, operands staged in the
 // interleaved K-major layout of tcgen05.cuh.  mode bit 0 swaps LBO/SBO (convention probe).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC -I paper_1804_10987_b200/csrc
+//        scripts/tc_probe.cu -o paper_1804_10987_b200/libtcprobe.so -lcuda
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "tcgen05.cuh"

@@ -59,3 +59,25 @@ def test_library_counters_match(mode, topology):
         got = pre.comm_ledger(reset=True)
     want = ledger.library_payload(1, n_sc, cfg.K, cfg.U, mode, topology=topology, s_on_all_ranks=False, comm=True)
     assert got == want, (got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("force_comm", [False, True])
+def test_prepare_pd_ledger_world1(force_comm):
+    """dp_prepare_pd counts the Gram exchange only when a collective is issued: nothing at
+    world 1 without a communicator, the packed Gram payload with a (forced) 1-rank one."""
+    import torch
+
+    from paper_1804_10987_b200 import CONFIGS, synth
+    from paper_1804_10987_b200 import _lib as L
+    from paper_1804_10987_b200.api import Precoder
+    cfg = CONFIGS[3]
+    n_sc = 7
+    f = synth.make_frame(cfg.cfg_id, n_sc, cfg.B, cfg.U, cfg.K, cfg.M)
+    kw = dict(flags=L.DP_FLAG_FORCE_COMM, nccl_id=L.dp_get_unique_id()) if force_comm else {}
+    with Precoder(n_sc, cfg.B, cfg.U, cfg.K, cfg.C, **kw) as pre:
+        pre.prepare_pd(torch.from_numpy(f.H).cuda(), 0.1, 1.0)
+        torch.cuda.synchronize()
+        got = pre.comm_ledger(reset=True)
+    want = n_sc * cfg.U * (cfg.U + 1) // 2 * 2 if force_comm else 0
+    assert got == {"gram": want, "s_bcast": 0, "z_bcast": 0, "scalars": 0}, got
