@@ -1,6 +1,7 @@
 """bench.py — precoded Gbit/s and frame latency (device-timed) of PD-WF and FD-WF.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4|fig2a..fig2e] [--K 7]
+                    [--impl ours|reference] [--mode both|pd|fd] [--fp64]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
 Workload (BASELINE.json configs[3]): B=256 antennas, U=32 UEs,
@@ -10,10 +11,12 @@ one PD-WF frame followed by one FD-WF frame, so
 bits/step = 2 * N_sc * K * U * log2(M) for the whole job.  Scaling is STRONG
 (the frame is fixed; clusters are sharded over the N GPUs, C/N per GPU).
 
-Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
-CUDA events on the launching stream, max over ranks.  Inputs rotate over R
-resident input sets whose total size exceeds 2x L2 (126 MB), so every step
-reads H from HBM.  Rank 0 prints ONE JSON line.
+Timing: W warm-up steps, then K steps (default 500 = 1000 frames, the steady
+state of SURVEY §8(d)) bracketed by barrier + synchronize, CUDA events on the
+launching stream, max over ranks.  Inputs rotate over R resident input sets
+whose total size exceeds 2x L2 (126 MB), so every step reads H from HBM.
+Single-frame latency p50 / p99 over 200 frames per precoder.  Rank 0 prints
+ONE JSON line.
 """
 from __future__ import annotations
 
@@ -33,21 +36,28 @@ sys.path.insert(0, ROOT)
 METRIC = "precoded Gbit/s and frame latency (device-timed) for PD/FD WF at 1/2/4/8 B200"
 L2_BYTES = 126 * 1024 * 1024
 SEED = 180410987
+# builder-measured FP32 FFMA pipe peak (scripts/ffma2_probe.cu on the B200 pool, committed under
+# profiles/); the fallback is the nominal clock product 148 SMs x 128 lanes x 2 flop x sm_max_mhz
+FP32_PEAK_FILE = os.path.join(ROOT, "profiles", "fp32_peak.json")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="4", help="4 (default), 2, 3 or a paper point fig2a..fig2e")
+    ap.add_argument("--K", type=int, default=0, help="override the symbols per frame (e.g. 7 to mirror the paper)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="both", choices=["both", "pd", "fd"])
     ap.add_argument("--unfused", action="store_true", help="three-kernel path (a)(b)(c)")
+    ap.add_argument("--fp64", action="store_true", help="DP_FLAG_FP64 accuracy option (fp64 accumulation)")
     ap.add_argument("--pd-topology", default="scatter_gather", choices=["allreduce", "reduce_bcast", "scatter_gather"],
                     help="PD exchange for N > 1 (DESIGN.md §6); scatter_gather splits the solve over the GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled oracle check at N > 1")
+    ap.add_argument("--latency-frames", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time for cpu_baseline")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no JSON extras)")
     ap.add_argument("--cluster-sizes", default="", help="comma list of C unequal cluster sizes B_c (dp_set_clusters, "
@@ -57,24 +67,58 @@ def parse():
     return ap.parse_args()
 
 
+def get_config(args):
+    from paper_1804_10987_b200 import CONFIGS, PAPER_POINTS
+    cfg = PAPER_POINTS[args.config] if args.config in PAPER_POINTS else CONFIGS[int(args.config)]
+    if args.K:
+        cfg = type(cfg)(cfg.cfg_id, f"{cfg.name}_K{args.K}", cfg.n_sc, cfg.B, cfg.U, cfg.C, args.K, cfg.M,
+                        cfg.snr_db, cfg.tau)
+    return cfg
+
+
 # ---------------------------------------------------------------- algorithmic work
 def flops_problem(U: int, nb: int, K: int) -> dict:
     """Algorithmic real flops of one WF problem (one subcarrier x one cluster for FD, one
     subcarrier over nb antennas for PD); complex MAC = 8 flops.
     Gram: Hermitian half U(U+1)/2 entries x nb ; Cholesky U^3/6 ; L^-1 U^3/6 ; A^-1 = W0^H W0 U^3/6 ;
-    whiten K U^2 ; precode K nb U."""
-    cmac = {
-        "gram": nb * U * (U + 1) / 2,
-        "solve": U ** 3 / 2,
-        "whiten": K * U * U,
-        "precode": K * nb * U,
-    }
+    whiten K U^2 ; precode K nb U.  For nb < U (FD branch B_c < U) the same terms in the
+    nb x nb space: Gram U nb(nb+1)/2, solve nb^3/2, H^H s K nb U, apply W K nb^2."""
+    if nb < U:
+        cmac = {"gram": U * nb * (nb + 1) / 2, "solve": nb ** 3 / 2, "whiten": K * nb * nb, "precode": K * nb * U}
+    else:
+        cmac = {"gram": nb * U * (U + 1) / 2, "solve": U ** 3 / 2, "whiten": K * U * U, "precode": K * nb * U}
     return {k: 8.0 * v for k, v in cmac.items()}
 
 
 def bytes_frame(cfg, Bl: int) -> dict:
     """Algorithmic HBM bytes per frame per GPU: H read once, s read once, x written once."""
     return {"H": cfg.n_sc * Bl * cfg.U * 8, "s": cfg.n_sc * cfg.K * cfg.U * 8, "x": cfg.n_sc * cfg.K * Bl * 8}
+
+
+def load_peaks():
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32 = {"tflops": 148 * 128 * 2 * sm_max * 1e6 / 1e12, "source": f"nominal: 148 SMs x 128 lanes x 2 x {sm_max:.0f} MHz"}
+    fp64 = {"tflops": fp32["tflops"] / 2, "source": "nominal: half the FP32 rate"}
+    try:
+        with open(FP32_PEAK_FILE) as f:
+            m = json.load(f)
+        fp32 = {"tflops": float(m["ffma_tflops"]), "source": f"builder-measured ({m['how']})"}
+        if "dfma_tflops" in m:
+            fp64 = {"tflops": float(m["dfma_tflops"]), "source": f"builder-measured ({m['how']})"}
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    bf16 = float(peaks.get("bf16_tflops", 1590.0))
+    # tf32 dense peak: the measured bf16 peak x the nominal tf32 / bf16 ratio (1.1 / 2.25 PFLOP/s)
+    tf32 = bf16 * 1.1 / 2.25
+    return {"fp32": fp32, "fp64": fp64, "hbm_gbs": hbm, "tf32_tflops": tf32,
+            "hbm_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
 
 
 # ---------------------------------------------------------------- clocks sampler
@@ -132,34 +176,36 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- oracle CPU baseline
-def _oracle_step(cfg, f, N0):
+def _oracle_step(cfg, f, N0, modes=("pd", "fd")):
     import oracle
 
-    oracle.pd(f.H, f.s, cfg.C, N0)
-    oracle.fd(f.H, f.s, cfg.C, N0, tau=cfg.tau)
+    if "pd" in modes:
+        oracle.pd(f.H, f.s, cfg.C, N0)
+    if "fd" in modes:
+        oracle.fd(f.H, f.s, cfg.C, N0, tau=cfg.tau)
 
 
-def cpu_baseline(cfg, target_s: float, chunk: int = 96):
+def cpu_baseline(cfg, target_s: float, modes, chunk: int = 96):
     """The fp64 oracle (oracle/, as it stands) on a bounded sample of the same workload:
-    a chunk of `chunk` subcarriers of one frame (PD + FD), repeated until ~target_s of
-    CPU work, on all host cores (OpenMP over subcarriers)."""
+    a chunk of `chunk` subcarriers of one frame (the bench's precoders), repeated until ~target_s
+    of CPU work, on all host cores (OpenMP over subcarriers)."""
     import oracle
     from paper_1804_10987_b200 import synth
 
     N0 = synth.n0_from_snr_db(cfg.snr_db)
     f = synth.make_frame(cfg.cfg_id, chunk, cfg.B, cfg.U, cfg.K, cfg.M, frame=77)
-    _oracle_step(cfg, f, N0)                      # warm (page-in, thread pool)
+    _oracle_step(cfg, f, N0, modes)               # warm (page-in, thread pool)
     reps, t0 = 0, time.perf_counter()
     while True:
-        _oracle_step(cfg, f, N0)
+        _oracle_step(cfg, f, N0, modes)
         reps += 1
         el = time.perf_counter() - t0
         if el >= target_s or reps >= 10000:
             break
-    bits = 2 * reps * chunk * cfg.K * cfg.U * (cfg.M.bit_length() - 1)
+    bits = len(modes) * reps * chunk * cfg.K * cfg.U * (cfg.M.bit_length() - 1)
     return {"value": bits / el / 1e9, "unit": "Gbit/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{reps} x {chunk} subcarriers of {cfg.name} (PD + FD frames, fp64 C oracle, "
-                      f"OpenMP over subcarriers), {el:.1f} s"}
+            "sample": f"{reps} x {chunk} subcarriers of {cfg.name} ({'+'.join(m.upper() for m in modes)} frames, "
+                      f"fp64 C oracle, OpenMP over subcarriers), {el:.1f} s"}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -172,33 +218,178 @@ def run_reference(args, cfg, rank, world):
     from paper_1804_10987_b200 import synth
 
     N0 = synth.n0_from_snr_db(cfg.snr_db)
+    modes = ["pd", "fd"] if args.mode == "both" else [args.mode]
     chunk = 48
     f = synth.make_frame(cfg.cfg_id, chunk, cfg.B, cfg.U, cfg.K, cfg.M, frame=78)
-    for _ in range(args.warmup):
-        _oracle_step(cfg, f, N0)
+    # bounded: the default 500 timed steps would run for minutes on the oracle; at most 20 steps
+    steps = min(args.steps, 20)
+    warm = min(args.warmup, 3)
+    for _ in range(warm):
+        _oracle_step(cfg, f, N0, modes)
     t = time.perf_counter()
-    for _ in range(args.steps):
-        _oracle_step(cfg, f, N0)
+    for _ in range(steps):
+        _oracle_step(cfg, f, N0, modes)
     el = time.perf_counter() - t
-    bits = 2 * chunk * cfg.K * cfg.U * (cfg.M.bit_length() - 1) * args.steps
+    bits = len(modes) * chunk * cfg.K * cfg.U * (cfg.M.bit_length() - 1) * steps
     v = bits / el / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gbit/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "steps": steps, "warmup": warm, "ms_per_step": el / steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "step": f"PD + FD frames on {chunk} of {cfg.n_sc} subcarriers"},
+            "config": {"workload": cfg.name, "step": f"{'+'.join(m.upper() for m in modes)} frames on {chunk} of "
+                                                      f"{cfg.n_sc} subcarriers",
+                       "steps_requested": args.steps},
             "cpu_baseline": {"value": v, "unit": "Gbit/s", "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": f"{chunk} of {cfg.n_sc} subcarriers per step, PD + FD"},
+                             "sample": f"{chunk} of {cfg.n_sc} subcarriers per step"},
             "e2e": {"value": v, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- roofline
+def fd_pipes(cfg, U, S, K, n_problems, kernel_path):
+    """Split the §8(d) algorithmic FD flops by the pipe each step runs on, for the kernel that ran."""
+    fl = flops_problem(U, S, K)
+    tot = {k: v * n_problems for k, v in fl.items()}
+    if kernel_path == "fd_tc+wtc":                   # Gram and whitening on tcgen05 (3xTF32)
+        tensor, simt = ["gram", "whiten"], ["solve", "precode"]
+    elif kernel_path == "fd_tc":
+        tensor, simt = ["gram"], ["solve", "whiten", "precode"]
+    else:
+        tensor, simt = [], ["gram", "solve", "whiten", "precode"]
+    return tot, sum(tot[k] for k in tensor), sum(tot[k] for k in simt), tensor, simt
+
+
+def roofline(cfg, world, prof, ms_prof, ms_step_unprof, steps, peaks, sizes, fp64, modes):
+    Bl = cfg.B // world
+    Cl = cfg.C // world
+    bf = bytes_frame(cfg, Bl)
+    fp32 = peaks["fp32"]["tflops"]
+    hbm = peaks["hbm_gbs"]
+    pipe = peaks["fp64"] if fp64 else peaks["fp32"]
+    npk = cfg.U * (cfg.U + 1) // 2 * 8
+    flp = flops_problem(cfg.U, Bl, cfg.K)
+    # which FD kernel ran (dp_api.cu dispatch): fd_tc at U = B_c = 32, K <= 16 (tensor-core whitening when
+    # a CTA's 4 problems share the subcarrier), the SIMT fused kernel otherwise, fd_f64 with --fp64
+    if fp64:
+        fd_path = "fd_f64"
+    elif cfg.U == 32 and cfg.S == 32 and cfg.K <= 16:
+        fd_path = "fd_tc+wtc" if Cl % 4 == 0 else "fd_tc"
+    else:
+        fd_path = "fd_fused" if cfg.S >= cfg.U else "fd_small"
+    per = {}
+    for k, v in prof.items():
+        if not v["launches"]:
+            continue
+        kms = v["ms"] / v["launches"]
+        e = {"ms_avg": kms, "launches": v["launches"]}
+        if k == "gram":
+            b = bf["H"] + cfg.n_sc * npk
+            e.update(bound="hbm", bytes=b, achieved_gbs=b / (kms / 1e3) / 1e9, frac=b / (kms / 1e3) / 1e9 / hbm)
+        elif k == "precode":
+            b = bf["H"] + bf["s"] + bf["x"]
+            e.update(bound="hbm", bytes=b, achieved_gbs=b / (kms / 1e3) / 1e9, frac=b / (kms / 1e3) / 1e9 / hbm)
+        elif k == "solve":
+            f_ = cfg.n_sc * (flp["solve"] + flp["whiten"])
+            e.update(bound="alu", flops=f_, achieved_tflops=f_ / (kms / 1e3) / 1e12,
+                     frac=f_ / (kms / 1e3) / 1e12 / pipe["tflops"],
+                     note="1 U x U problem per subcarrier: latency-bound (SURVEY §8(d): reported, not graded)")
+        elif k == "fused_fd" and not sizes:
+            tot, tflops, sflops, tn, sn = fd_pipes(cfg, cfg.U, cfg.S, cfg.K, cfg.n_sc * Cl, fd_path)
+            allf = sum(tot.values())
+            b = bf["H"] + bf["s"] + bf["x"]
+            t = kms / 1e3
+            e.update(bound="alu", kernel_path=fd_path, method_flops=allf,
+                     achieved_tflops=allf / t / 1e12, frac=allf / t / 1e12 / pipe["tflops"],
+                     pipes={"simt_steps": sn, "simt_flops": sflops, "simt_frac": sflops / t / 1e12 / pipe["tflops"],
+                            "tensor_steps": tn, "tensor_flops_3xtf32": 3 * tflops,
+                            "tensor_frac": 3 * tflops / t / 1e12 / peaks["tf32_tflops"],
+                            "hbm_bytes": b, "hbm_frac": b / t / 1e9 / hbm})
+        else:
+            e.update(bound="latency", note="per-subcarrier scalar combine")
+        per[k] = e
+    # dominant kernel (or the whole FD frame for unequal clusters: its runs overlap on streams)
+    if sizes:
+        fl_tot = 0.0
+        for bc in sizes[cfg.C // world * 0: cfg.C // world * 0 + Cl] if world > 1 else sizes:
+            fl_tot += sum(flops_problem(cfg.U, bc, cfg.K).values()) * cfg.n_sc
+        t = ms_step_unprof / 1e3
+        return {"bound": "alu", "achieved": fl_tot / t / 1e12, "peak": pipe["tflops"], "unit": "TFLOP/s",
+                "frac": fl_tot / t / 1e12 / pipe["tflops"], "traffic": None, "kernel": "fd_frame(unequal runs)",
+                "kernel_ms_avg": ms_step_unprof, "kernel_share_of_step": 1.0,
+                "kernel_timing": "unprofiled FD frame time (its runs overlap on up to 3 streams)",
+                "algorithmic_flops_per_launch": fl_tot, "peak_note": pipe["source"], "per_kernel": per}
+    dom = max(per, key=lambda k: per[k]["ms_avg"] * per[k]["launches"])
+    d = per[dom]
+    share = prof[dom]["ms"] / max(ms_prof, 1e-9)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"{cfg.name}/{dom}/n{world}")
+    except Exception:
+        pass
+    timing = ("CUDA events around each launch on its stream, in a second pass of the same "
+              f"{steps} steps (profiled step {ms_prof / steps:.4f} ms vs {ms_step_unprof:.4f} ms unprofiled: events "
+              "between kernels break the PDL overlap)")
+    if d["bound"] == "hbm":
+        r = {"bound": "hbm", "achieved": d["achieved_gbs"], "peak": hbm, "unit": "GB/s", "frac": d["frac"],
+             "algorithmic_bytes_per_launch": d["bytes"], "peak_note": peaks["hbm_source"]}
+    else:
+        f_ = d.get("method_flops", d.get("flops", 0.0))
+        r = {"bound": "alu", "achieved": f_ / (d["ms_avg"] / 1e3) / 1e12, "peak": pipe["tflops"], "unit": "TFLOP/s",
+             "frac": f_ / (d["ms_avg"] / 1e3) / 1e12 / pipe["tflops"], "algorithmic_flops_per_launch": f_,
+             "algorithmic_bytes_per_launch": bf["H"] + bf["s"] + bf["x"],
+             "peak_note": ("FP64 DFMA pipe, " if fp64 else "FP32 FFMA pipe, ") + pipe["source"] +
+                          "; achieved = the §8(d) whole-method flops of the launch (Gram + solve + whitening + "
+                          "precode, wherever each runs) / its time; per_kernel[...].pipes splits them by pipe"}
+    r.update(traffic=traffic, kernel=dom, kernel_ms_avg=d["ms_avg"], kernel_share_of_step=share,
+             kernel_timing=timing, per_kernel=per)
+    return r
+
+
+# ---------------------------------------------------------------- N > 1: sampled parity vs the oracle
+def parity_check(pre, cfg, world, rank, dev, Hs, Ss, modes, N0, nsamp=8):
+    """Verification leg (not on the product path): every rank precodes one resident input set, the
+    sampled subcarriers' H_local / x_local are gathered to rank 0, which recomputes them with the fp64
+    oracle (subcarriers are independent).  Reported as relative L2 per precoder."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    idx = torch.linspace(0, cfg.n_sc - 1, nsamp, device=dev).round().long()
+    out = {}
+    for m in modes:
+        x = (pre.precode_pd if m == "pd" else pre.precode_fd)(Hs[0], Ss[0], N0, 1.0)
+        torch.cuda.synchronize(dev)
+        hs = Hs[0][idx].contiguous()
+        xs = x[idx].contiguous()
+        if world > 1:
+            hp = [torch.empty_like(hs) for _ in range(world)]
+            xp = [torch.empty_like(xs) for _ in range(world)]
+            dist.all_gather(hp, hs)
+            dist.all_gather(xp, xs)
+            hs, xs = torch.cat(hp, dim=1), torch.cat(xp, dim=2)
+        if rank == 0:
+            import oracle
+            H = hs.cpu().numpy()
+            s = Ss[0][idx].cpu().numpy()
+            if m == "pd":
+                xr, _ = oracle.pd(H, s, cfg.C, N0)
+            else:
+                xr, _ = oracle.fd(H, s, cfg.C, N0, tau=cfg.tau)
+            xg = xs.cpu().numpy().astype(np.complex128)
+            out[m] = float(np.linalg.norm(xg - xr) / np.linalg.norm(xr))
+    if rank == 0:
+        out["subcarriers"] = [int(v) for v in idx.tolist()]
+        out["tol"] = 1e-4
+        out["ok"] = all(out[m] <= 1e-4 for m in modes)
+    return out
+
+
 # ---------------------------------------------------------------- ours
 def main():
     args = parse()
-    from paper_1804_10987_b200 import CONFIGS
-    cfg = CONFIGS[args.config]
+    cfg = get_config(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -225,21 +416,23 @@ def main():
     Bl = cfg.B // world
     N0 = synth.n0_from_snr_db(cfg.snr_db)
 
-    # NCCL id for the library's own communicator
     # Two contexts: `pre` times `value` with nothing between the kernels (events between
     # launches would break the programmatic-dependent-launch overlap), `pre_prof`
     # (DP_FLAG_PROFILE: CUDA events around every kernel, on the launching stream) runs the
     # same steps right after it for the per-kernel times of the roofline.
-    flags = L.DP_FLAG_UNFUSED if args.unfused else 0
-    pre = Precoder(cfg.n_sc, cfg.B, cfg.U, cfg.K, cfg.C, rank=rank, world=world, device=local, tau=cfg.tau,
-                   pd_topology=args.pd_topology, s_on_all_ranks=(world == 1), flags=flags,
-                   nccl_id=D.bootstrap_nccl_id() if world > 1 else None)
-    pre_prof = Precoder(cfg.n_sc, cfg.B, cfg.U, cfg.K, cfg.C, rank=rank, world=world, device=local, tau=cfg.tau,
-                        pd_topology=args.pd_topology, s_on_all_ranks=(world == 1), flags=flags | L.DP_FLAG_PROFILE,
-                        nccl_id=D.bootstrap_nccl_id() if world > 1 else None)
+    flags = (L.DP_FLAG_UNFUSED if args.unfused else 0) | (L.DP_FLAG_FP64 if args.fp64 else 0)
+    mk = lambda fl: Precoder(cfg.n_sc, cfg.B, cfg.U, cfg.K, cfg.C, rank=rank, world=world, device=local,  # noqa: E731
+                             tau=cfg.tau, pd_topology=args.pd_topology, s_on_all_ranks=(world == 1), flags=fl,
+                             nccl_id=D.bootstrap_nccl_id() if world > 1 else None)
+    pre = mk(flags)
+    pre_prof = mk(flags | L.DP_FLAG_PROFILE)
 
     sizes = [int(v) for v in args.cluster_sizes.split(",")] if args.cluster_sizes else None
     if sizes:
+        if len(sizes) != cfg.C:
+            raise SystemExit(f"--cluster-sizes needs C={cfg.C} entries, got {len(sizes)}")
+        if args.mode != "fd":
+            raise SystemExit("--cluster-sizes applies to FD only: use --mode fd")
         for p_ in (pre, pre_prof):
             p_.set_clusters(sizes, [b / cfg.B for b in sizes])
 
@@ -248,7 +441,7 @@ def main():
     per_set = bf["H"] + bf["s"] + bf["x"]
     R = max(2, math.ceil(2 * L2_BYTES / per_set))
     gen = torch.Generator(device=dev)
-    gen.manual_seed(SEED + 1000 * args.config + rank)
+    gen.manual_seed(SEED + 1000 * cfg.cfg_id + rank)
     pts = torch.from_numpy(synth.QAM(cfg.M).points().astype("complex64")).to(dev)
     Hs, Ss, Xs = [], [], []
     for r in range(R):
@@ -294,6 +487,7 @@ def main():
     # launches carry their PDL attributes into programmatic graph edges; NCCL calls are capturable)
     # and replayed, or launched eagerly (--eager, or if capture is refused)
     launches0 = pre.launch_count()
+    pre.comm_ledger(reset=True)
     graph, launch_mode = None, "eager"
     if not args.eager:
         try:
@@ -308,6 +502,7 @@ def main():
             launch_mode = f"eager (graph capture failed: {str(e)[:120]})"
             barrier()
     launches = pre.launch_count() - launches0
+    ledger = pre.comm_ledger(reset=True)                 # payload of the captured (= timed) steps
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         barrier()
@@ -322,6 +517,8 @@ def main():
     ms = ev0.elapsed_time(ev1)
     if graph is None:
         launches = pre.launch_count() - launches0
+        ledger = pre.comm_ledger(reset=True)
+    del graph
     # per-kernel times: the same K steps again through the profiling context
     barrier()
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -332,20 +529,17 @@ def main():
     barrier()
     ms_prof = pe0.elapsed_time(pe1)
     prof = pre_prof.profile(reset=True)
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = D.max_over_ranks(ms, dev)
     bits_frame = cfg.bits_per_frame
     bits_step = bits_frame * len(modes)
     value = bits_step * args.steps / (ms_max / 1e3) / 1e9
 
-    # ---------------- per-mode single-frame latency (p50 / p99 over 40 frames each)
+    # ---------------- per-mode single-frame latency (p50 / p99 over --latency-frames frames each)
     lat = {}
     for m in modes:
         fn = pre.precode_pd if m == "pd" else pre.precode_fd
         xs = []
-        for i in range(40):
+        for i in range(args.latency_frames):
             j = i % R
             barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -353,14 +547,11 @@ def main():
             fn(Hs[j], Ss[j], N0, 1.0, out=Xs[j])
             b.record(stream)
             torch.cuda.synchronize(dev)
-            tt = torch.tensor([a.elapsed_time(b)], device=dev)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            xs.append(float(tt.item()))
+            xs.append(D.max_over_ranks(a.elapsed_time(b), dev))
         xs.sort()
         p50 = xs[len(xs) // 2]
         lat[m] = {"latency_ms_p50": p50, "latency_ms_p99": xs[min(len(xs) - 1, int(0.99 * len(xs)))],
-                  "gbps_at_p50": bits_frame / (p50 / 1e3) / 1e9}
+                  "frames": len(xs), "gbps_at_p50": bits_frame / (p50 / 1e3) / 1e9}
     pre.profile(reset=True)
 
     # ---------------- e2e through the C-ABI with pinned HOST buffers (H2D + compute + D2H per call)
@@ -380,122 +571,49 @@ def main():
                 (pre.precode_pd if m == "pd" else pre.precode_fd)(Hh, Sh, N0, 1.0, out=Xh)
         e1.record(stream)
         barrier()
-        et = torch.tensor([e0.elapsed_time(e1)], device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item())
+        e_ms = D.max_over_ranks(e0.elapsed_time(e1), dev)
         e2e = {"value": bits_step * ne / (e_ms / 1e3) / 1e9, "unit": "Gbit/s",
                "h2d_bytes_per_step": len(modes) * (bf["H"] + bf["s"]),
                "d2h_bytes_per_step": len(modes) * bf["x"], "ms_per_step": e_ms / ne,
                "note": "pinned host H, s, x through dp_precode_*: H2D, kernels, D2H inside each call"}
         pre.profile(reset=True)
 
-    # ---------------- roofline of the dominant kernel (measured in the timed region)
-    dom = max(prof, key=lambda k: prof[k]["ms"])
-    dom_ms = prof[dom]["ms"] / max(prof[dom]["launches"], 1)
-    step_ms_local = ms / args.steps
-    share = prof[dom]["ms"] / max(ms_prof, 1e-9)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:
-        pass
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12            # TFLOP/s, FFMA pipe
-    Cl = cfg.C // world
-    if dom == "fused_fd":
-        # U = 32: the cluster Gram runs on the tensor cores (fd_tc.cuh), so the FP32-pipe
-        # roofline counts the SIMT steps only (solve + whiten + precode); the Gram's flops are
-        # reported beside it (tensor-core time at its 3xTF32 rate is ~3 us, not the bound).
-        fl = flops_problem(cfg.U, cfg.S, cfg.K)
-        simt = fl["solve"] + fl["whiten"] + fl["precode"] + (0.0 if cfg.U == 32 else fl["gram"])
-        flops_launch = cfg.n_sc * Cl * simt
-        bytes_launch = bf["H"] + bf["s"] + bf["x"]
-    else:
-        # PD kernels (a) gram: H -> packed G ; (b) solve: G, s -> z ; (c) precode: H, z -> x
-        fl = flops_problem(cfg.U, Bl, cfg.K)
-        npk = cfg.U * (cfg.U + 1) // 2 * 8
-        flops_launch = cfg.n_sc * {"gram": fl["gram"], "solve": fl["solve"] + fl["whiten"],
-                                   "precode": fl["precode"]}.get(dom, sum(fl.values()))
-        bytes_launch = {"gram": bf["H"] + cfg.n_sc * npk,
-                        "solve": cfg.n_sc * npk + bf["s"] + bf["s"],
-                        "precode": bf["H"] + bf["s"] + bf["x"]}.get(dom, bf["H"])
-    achieved = flops_launch / (dom_ms / 1e3) / 1e12
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        traffic = tr.get(f"{cfg.name}/{dom}/n{world}")
-    except Exception:
-        pass
-    roof = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp32_peak, "traffic": traffic, "kernel": dom,
-            "kernel_ms_avg": dom_ms, "kernel_share_of_step": share,
-            "kernel_timing": "CUDA events around each launch on its stream, in a second pass of the same "
-                             f"{args.steps} steps (profiled step {ms_prof / args.steps:.4f} ms vs {ms / args.steps:.4f} ms "
-                             "unprofiled: events between kernels break the PDL overlap)",
-            "algorithmic_flops_per_launch": flops_launch, "algorithmic_bytes_per_launch": bytes_launch,
-            "hbm_achieved_gbs": bytes_launch / (dom_ms / 1e3) / 1e9,
-            "hbm_peak_gbs": peaks.get("hbm_gbs", 6544.0),
-            "peak_note": f"FP32 FFMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json); achieved counts the SIMT steps (solve + whiten + precode), the U=32 cluster Gram runs on the tensor cores",
-            "kernels": {k: {"ms_avg": v["ms"] / max(v["launches"], 1), "launches": v["launches"]}
-                        for k, v in prof.items() if v["launches"]}}
+    peaks = load_peaks()
+    roof = roofline(cfg, world, prof, ms_prof, ms / args.steps, args.steps, peaks, sizes, args.fp64, modes)
 
-    # every kernel against its own bound: gram / precode move H through HBM with
-    # the contraction on the tensor cores (bound "hbm"); solve and the FD kernel are FP32-pipe work
-    hbm_peak = float(peaks.get("hbm_gbs", 6544.0))
-    flp = flops_problem(cfg.U, Bl, cfg.K)
-    flf = flops_problem(cfg.U, cfg.S, cfg.K)
-    npk = cfg.U * (cfg.U + 1) // 2 * 8
-    per = {}
-    for k, v in prof.items():
-        if not v["launches"]:
-            continue
-        kms = v["ms"] / v["launches"]
-        if k == "gram":
-            b = bf["H"] + cfg.n_sc * npk
-            per[k] = {"bound": "hbm", "bytes": b, "achieved_gbs": b / (kms / 1e3) / 1e9, "frac": b / (kms / 1e3) / 1e9 / hbm_peak}
-        elif k == "precode":
-            b = bf["H"] + bf["s"] + bf["x"]
-            per[k] = {"bound": "hbm", "bytes": b, "achieved_gbs": b / (kms / 1e3) / 1e9, "frac": b / (kms / 1e3) / 1e9 / hbm_peak}
-        elif k == "solve":
-            f_ = cfg.n_sc * (flp["solve"] + flp["whiten"])
-            per[k] = {"bound": "alu", "flops": f_, "achieved_tflops": f_ / (kms / 1e3) / 1e12,
-                      "frac": f_ / (kms / 1e3) / 1e12 / fp32_peak,
-                      "note": "1 U x U problem per subcarrier: latency-bound (SURVEY §8(d))"}
-        elif k == "fused_fd":
-            simt = flf["solve"] + flf["whiten"] + flf["precode"] + (0.0 if cfg.U == 32 else flf["gram"])
-            f_ = cfg.n_sc * Cl * simt
-            per[k] = {"bound": "alu", "flops": f_, "achieved_tflops": f_ / (kms / 1e3) / 1e12,
-                      "frac": f_ / (kms / 1e3) / 1e12 / fp32_peak,
-                      "tensor_core_gram_flops": cfg.n_sc * Cl * flf["gram"] if cfg.U == 32 else 0.0}
-        else:                                    # fd_finish_kernel (U < 32): per-subcarrier scalars
-            per[k] = {"bound": "latency", "note": "tiny per-subcarrier combine"}
-        per[k]["ms_avg"] = kms
-    roof["per_kernel"] = per
+    parity = None
+    if world > 1 and not args.no_parity:
+        parity = parity_check(pre, cfg, world, rank, dev, Hs, Ss, modes, N0)
+    comm = pre.comm_info()
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(cfg, args.cpu_seconds)
+        cpu = cpu_baseline(cfg, args.cpu_seconds, modes)
 
     clocks = clk.summary()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "complex64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64-accumulate, complex64 I/O" if args.fp64 else "complex64",
+            "data": "synthetic",
             "config": {"workload": f"{cfg.name}: B={cfg.B} U={cfg.U} C={cfg.C} S={cfg.S} N_sc={cfg.n_sc} "
                                    f"K={cfg.K} {cfg.M}-QAM SNR={cfg.snr_db} dB tau={cfg.tau}",
                        "step": "+".join(m.upper() + "-WF frame" for m in modes),
-                       "bits_per_step": bits_step, "clusters_per_gpu": Cl,
+                       "bits_per_step": bits_step, "clusters_per_gpu": cfg.C // world,
                        **({"cluster_sizes": sizes} if sizes else {}),
                        "parallelism": f"cluster-sharded x{world}" + ("" if world == 1 else f", PD {args.pd_topology}"),
                        "l2": f"{R} rotating resident input sets of {per_set / 2**20:.1f} MiB (> 2x L2)",
-                       "path": "unfused (a)(b)(c)" if args.unfused else "fused single pass",
+                       "path": ("fp64 accumulation (DP_FLAG_FP64)" if args.fp64 else
+                                "unfused (a)(b)(c)" if args.unfused else "fused single pass"),
                        "launch": launch_mode},
             "modes": lat,
             "roofline": roof,
+            "comm": {"bytes_per_step": 4 * sum(ledger.values()) / args.steps,
+                     "by_kind_bytes_per_step": {k: 4 * v / args.steps for k, v in ledger.items()},
+                     "nccl_nranks": comm["nranks"], "nccl_version": comm["nccl_version"],
+                     "note": "payload this rank handed to NCCL per step (dp_comm_ledger), rank 0"},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,

@@ -87,6 +87,16 @@ extern "C" {
 #define DP_FLAG_PROFILE     4  /* bracket every kernel launch with CUDA events (dp_profile_read)        */
 #define DP_FLAG_FORCE_COMM  8  /* world == 1: still issue the NCCL collectives (tests the comm path);
                                   requires nccl_id                                                     */
+#define DP_FLAG_FP64       16  /* accuracy option (SURVEY.md §8(b) "DP_GRAM_FP64"): Gram,
+                                  regularised solve, beta, whitening and precode accumulate in fp64
+                                  (H, s, x stay complex64).  For square clusters (B_c = U) at high SNR
+                                  or N0 = 0 (the ZF limit), where cond(G_c) of 1e4..1e9 puts the
+                                  fp32 path above the 1e-4 bar.  FD needs B_c >= U (the B_c < U branch
+                                  is well conditioned and stays fp32-only: DP_ERR_UNSUPPORTED); PD uses
+                                  the allreduce exchange (ncclDouble) whatever pd_topology says;
+                                  DP_FLAG_UNFUSED does not apply; prepare / apply: DP_ERR_UNSUPPORTED.
+                                  Slower than the default path (fp64 FMAs run at half the fp32 rate
+                                  and no tensor cores are used)                                       */
 
 /* dp_config.pd_topology */
 #define DP_PD_ALLREDUCE     0  /* allreduce packed G; every rank solves redundantly (default)          */
@@ -208,6 +218,11 @@ DP_API int dp_profile_read(dp_ctx *ctx, double *ms /*[DP_NUM_KERNELS]*/,
 
 /* Total kernels launched by this context since dp_init (all kinds). */
 DP_API long long dp_launch_count(dp_ctx *ctx);
+
+/* The context's communicator: *nranks = ranks of its NCCL communicator (0 when the context has
+ * none: world == 1 without DP_FLAG_FORCE_COMM), *nccl_version = the linked NCCL's version code
+ * (ncclGetVersion, e.g. 22809).  Either pointer may be NULL.  DP_ERR_INVALID for a NULL ctx. */
+DP_API int dp_comm_info(dp_ctx *ctx, int *nranks, int *nccl_version);
 
 /* Destroy the communicator and free all workspace.  Does not touch caller
  * buffers or streams.  NULL is accepted. */

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DP_LIB_PATH") or os.path.join(_HERE, "libdp.so")   # override: A/B experiments
 
 DP_OK, DP_ERR_NUMERIC, DP_ERR_INVALID, DP_ERR_CUDA, DP_ERR_NCCL, DP_ERR_UNSUPPORTED = range(6)
-DP_FLAG_SYNC, DP_FLAG_UNFUSED, DP_FLAG_PROFILE, DP_FLAG_FORCE_COMM = 1, 2, 4, 8
+DP_FLAG_SYNC, DP_FLAG_UNFUSED, DP_FLAG_PROFILE, DP_FLAG_FORCE_COMM, DP_FLAG_FP64 = 1, 2, 4, 8, 16
 DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST, DP_PD_SCATTER_GATHER = 0, 1, 2
 DP_SCALAR_BETA, DP_SCALAR_RX, DP_SCALAR_POWER = 0, 1, 2
 COMM_KINDS = ["gram", "s_bcast", "z_bcast", "scalars"]   # DP_COMM_* order
@@ -27,7 +27,7 @@ EXPORTS = [
     "dp_status", "dp_profile_read", "dp_launch_count", "dp_finalize", "dp_last_error",
     "dp_debug_gram", "dp_debug_solve", "dp_synth_frame", "dp_receive_count",
     "dp_prepare_pd", "dp_prepare_fd", "dp_apply", "dp_comm_ledger", "dp_precode_mrt", "dp_prepare_from_gram",
-    "dp_set_clusters",
+    "dp_set_clusters", "dp_comm_info",
 ]
 
 
@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
     L.dp_apply.argtypes = [P, P, P, I, P, P]
     L.dp_prepare_from_gram.argtypes = [P, I, P, D, D, P]
     L.dp_set_clusters.argtypes = [P, P, P, P]
+    L.dp_comm_info.argtypes = [P, P, P]
     U64 = ctypes.c_ulonglong
     L.dp_synth_frame.argtypes = [U64, U64, I, I, I, I, I, D, P, P, P, P, P]
     L.dp_receive_count.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P]
@@ -148,6 +149,13 @@ def dp_profile_read(ctx, reset: bool = False):
 
 def dp_launch_count(ctx) -> int:
     return int(lib().dp_launch_count(ctx))
+
+
+def dp_comm_info(ctx) -> tuple[int, int]:
+    """(ranks of the context's NCCL communicator or 0, linked NCCL version code)."""
+    n, v = ctypes.c_int(0), ctypes.c_int(0)
+    check(lib().dp_comm_info(ctx, ctypes.byref(n), ctypes.byref(v)), "dp_comm_info")
+    return n.value, v.value
 
 
 def dp_finalize(ctx) -> int:

@@ -162,6 +162,11 @@ class Precoder:
         """fp32 payload elements this rank handed to each collective kind (include/dp.h DP_COMM_*)."""
         return L.dp_comm_ledger(self.ctx, reset)
 
+    def comm_info(self) -> dict:
+        """{'nranks': ranks of the library's NCCL communicator (0: none), 'nccl_version': code}."""
+        n, v = L.dp_comm_info(self.ctx)
+        return {"nranks": n, "nccl_version": v}
+
     def launch_count(self) -> int:
         return L.dp_launch_count(self.ctx)
 

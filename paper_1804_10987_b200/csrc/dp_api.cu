@@ -78,6 +78,15 @@ int validate_call(dp_ctx *c, const void *H, const void *s, double N0, double rho
   return DP_OK;
 }
 
+// regulariser kappa and Lemma-1 coefficient Es / rho_x^2 of a call (fp32 for the default kernels,
+// fp64 for the DP_FLAG_FP64 ones)
+void set_params(Args &a, double kappa, double coef) {
+  a.kappa = (float)kappa;
+  a.coef = (float)coef;
+  a.kappa64 = kappa;
+  a.coef64 = coef;
+}
+
 Args base_args(dp_ctx *c) {
   Args a;
   memset(&a, 0, sizeof(a));
@@ -177,6 +186,7 @@ int need_split(const dp_ctx *c) {
 int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, double rho2, float2 *xd, bool mrt,
                 cudaStream_t st) {
   const dp_config &k = c->cfg;
+  const bool fp64 = (k.flags & DP_FLAG_FP64) != 0;
   const size_t n = (size_t)k.n_sc * c->Cl;
   float *vb = c->vb;                                      // allocated by dp_set_clusters (no allocation here)
   dpk::VarRuns vr;
@@ -206,14 +216,15 @@ int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, dou
     a.S = r.S;
     a.nchunks = r.len;
     a.nbeta = r.len;
-    a.kappa = (float)(r.tau * k.U * N0 / rho_c2);         // Eq. 9 with the cluster's tau_c, rho_c^2
-    a.coef = (float)(k.Es / rho_c2);
+    set_params(a, (r.tau * k.U * N0 / rho_c2), (k.Es / rho_c2));  // Eq. 9 with the cluster's tau_c, rho_c^2
     a.beta = vb + (size_t)k.n_sc * r.cl0;
     a.pw = vb + n + (size_t)k.n_sc * r.cl0;
     a.fold = 0;
     vr.cl0[i] = r.cl0;
     vr.len[i] = r.len;
     if (mrt) rc = launch_mrt_u(c, a, sr);
+    else if (fp64 && r.S < k.U) rc = fail(DP_ERR_UNSUPPORTED, "DP_FLAG_FP64: FD branch B_c < U is fp32 only");
+    else if (fp64) rc = launch_fd_f64(c, a, sr);
     else if (r.S < k.U) rc = launch_fd_small(c, a, sr);
     else if (fd_tc_ok(c, a)) rc = launch_fd_tc_kc(c, a, sr);
     else rc = launch_fd_fused_any(c, a, sr);
@@ -242,12 +253,17 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   a.x = xd;
   a.S = c->S;
   a.nchunks = c->Cl;
-  a.kappa = (float)(k.tau * k.U * N0 / rho_c2);
-  a.coef = (float)(k.Es / rho_c2);
+  set_params(a, (k.tau * k.U * N0 / rho_c2), (k.Es / rho_c2));
   a.nbeta = c->Cl;
   if (!c->vruns.empty()) {
-    if (k.flags & DP_FLAG_UNFUSED) return fail(DP_ERR_UNSUPPORTED, "DP_FLAG_UNFUSED with unequal clusters");
+    if ((k.flags & DP_FLAG_UNFUSED) && !(k.flags & DP_FLAG_FP64))
+      return fail(DP_ERR_UNSUPPORTED, "DP_FLAG_UNFUSED with unequal clusters");
     RET(fd_var_runs(c, Hd, s_use, N0, rho2, xd, false, st));
+  } else if (k.flags & DP_FLAG_FP64) {
+    // accuracy option: the whole per-cluster chain with fp64 accumulation (f64.cuh)
+    if (c->S < k.U) return fail(DP_ERR_UNSUPPORTED, "DP_FLAG_FP64: FD branch B_c < U is fp32 only");
+    RET(launch_fd_f64(c, a, st));
+    RET(launch_fd_finish(c, a, st));
   } else if (c->S < k.U) {
     // small clusters (B_c < U): B_c x B_c regularised Gram per cluster
     RET(launch_fd_small(c, a, st));
@@ -301,7 +317,7 @@ int precode_mrt_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, do
   a.x = xd;
   a.S = c->S;
   a.nchunks = c->Cl;
-  a.coef = (float)(k.Es / (rho2 / k.C));                  // Es / rho_c^2, rho_c^2 = rho^2 / C
+  set_params(a, 0.0, k.Es / (rho2 / k.C));                // Es / rho_c^2, rho_c^2 = rho^2 / C
   a.nbeta = c->Cl;
   if (!c->vruns.empty()) {
     RET(fd_var_runs(c, Hd, s_use, 0.0, rho2, xd, true, st));
@@ -328,11 +344,32 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   a.x = xd;
   a.S = c->pd_chunk;
   a.nchunks = c->pd_nchunks;
-  a.kappa = (float)(k.U * N0 / rho2);
-  a.coef = (float)(k.Es / rho2);
+  set_params(a, (k.U * N0 / rho2), (k.Es / rho2));
   a.groups = 1;
   a.nbeta = 1;
   a.fin_inv_beta = (k.rank == 0) ? 1 : 0;   // 1/beta contributed once to the scalar allreduce
+  if (k.flags & DP_FLAG_FP64) {
+    // accuracy option (f64.cuh): fp64 partial Gram -> allreduce (ncclDouble) -> fp64 solve and
+    // whitening on every rank -> fp64-accumulated local precode
+    const float2 *s_use = sd;
+    RET(distribute_s(c, sd, st, &s_use));
+    a.s = s_use;
+    RET(launch_gram_f64(c, a, c->G64, st));
+    if (c->comm_on) {
+      const size_t n64 = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
+      NK(ncclAllReduce(c->G64, c->G64, n64, ncclDouble, ncclSum, c->comm, st));
+      LEDGER(c, DP_COMM_GRAM, 2 * n64);                   // fp32-sized units: one double = two floats
+    }
+    RET(launch_solve_f64(c, a, c->G64, c->z64, st));
+    RET(launch_precode_f64(c, a, c->z64, st));
+    if (c->comm_on) {
+      NK(ncclAllReduce(c->fin, c->fin, (size_t)k.n_sc * 2, ncclFloat, ncclSum, c->comm, st));
+      LEDGER(c, DP_COMM_SCALARS, (size_t)k.n_sc * 2);
+    }
+    c->last_mode = 0;
+    c->prepared = -1;
+    return DP_OK;
+  }
   const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
   const bool topo_t3 = c->comm_on && k.pd_topology == DP_PD_SCATTER_GATHER;
   const float2 *s_use = sd;
@@ -573,6 +610,10 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   A((void **)&c->fin, n_sc * 2 * 4);
   A((void **)&c->bad, 4);
   A((void **)&c->rd_buf, n_sc * 4);
+  if (k.flags & DP_FLAG_FP64) {
+    A((void **)&c->G64, n_sc * NP * 16);
+    A((void **)&c->z64, n_sc * k.K * k.U * 16);
+  }
   if (rc != DP_OK) {
     std::string e = g_err;
     dp_finalize(c);
@@ -659,6 +700,17 @@ int dp_profile_read(dp_ctx *c, double *ms, long long *launches, int reset) {
 }
 
 long long dp_launch_count(dp_ctx *c) { return c ? c->launches : 0; }
+
+int dp_comm_info(dp_ctx *c, int *nranks, int *nccl_version) {
+  g_err.clear();
+  if (!c) return fail(DP_ERR_INVALID, "ctx is NULL");
+  if (nranks) {
+    *nranks = 0;
+    if (c->comm) NK(ncclCommCount(c->comm, nranks));
+  }
+  if (nccl_version) NK(ncclGetVersion(nccl_version));
+  return DP_OK;
+}
 
 int dp_comm_ledger(dp_ctx *c, long long *floats, int reset) {
   g_err.clear();
@@ -760,7 +812,7 @@ int dp_finalize(dp_ctx *c) {
     if (c->ev_join[j]) cudaEventDestroy(c->ev_join[j]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev, c->vb, c->rd_buf};
+  void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev, c->vb, c->rd_buf, c->G64, c->z64};
   for (void *b : bufs)
     if (b) cudaFree(b);
   delete c;
@@ -801,8 +853,7 @@ int dp_debug_solve(dp_ctx *c, const dp_c32 *G, int groups, const dp_c32 *s, doub
   a.groups = groups;
   a.zout = reinterpret_cast<float2 *>(z);
   a.beta = beta;
-  a.kappa = (float)kappa;
-  a.coef = (float)(c->cfg.Es / rho_x2);
+  set_params(a, kappa, c->cfg.Es / rho_x2);
   RET(launch_solve_any(c, a, st));
   return DP_OK;
 }
@@ -821,11 +872,9 @@ int prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G, double N0, double rho2
   Args a = base_args(c);
   if (fd) {
     const double rho_c2 = rho2 / k.C;
-    a.kappa = (float)(k.tau * k.U * N0 / rho_c2);          // Eq. 9
-    a.coef = (float)(k.Es / rho_c2);
+    set_params(a, (k.tau * k.U * N0 / rho_c2), (k.Es / rho_c2));  // Eq. 9
   } else {
-    a.kappa = (float)(k.U * N0 / rho2);                    // Eq. 5
-    a.coef = (float)(k.Es / rho2);
+    set_params(a, (k.U * N0 / rho2), (k.Es / rho2));  // Eq. 5
     if (c->comm_on) {
       NK(ncclAllReduce(c->G, c->G, nG * 2, ncclFloat, ncclSum, c->comm, st));
       LEDGER(c, DP_COMM_GRAM, nG * 2);
@@ -844,6 +893,7 @@ int prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G, double N0, double rho2
 int dp_prepare_pd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stream) {
   g_err.clear();
   if (!c || !H) return fail(DP_ERR_INVALID, "ctx and H_local must be non-NULL");
+  if (c->cfg.flags & DP_FLAG_FP64) return fail(DP_ERR_UNSUPPORTED, "prepare / apply: not with DP_FLAG_FP64");
   if (!is_device_ptr(H)) return fail(DP_ERR_INVALID, "dp_prepare_pd takes device pointers");
   if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
   if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");
@@ -854,8 +904,7 @@ int dp_prepare_pd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
   a.H = reinterpret_cast<const float2 *>(H);
   a.S = c->pd_chunk;
   a.nchunks = c->pd_nchunks;
-  a.kappa = (float)(k.U * N0 / rho2);                      // Eq. 5
-  a.coef = (float)(k.Es / rho2);
+  set_params(a, (k.U * N0 / rho2), (k.Es / rho2));  // Eq. 5
   a.groups = 1;
   a.nbeta = 1;
   a.Gout = c->G;
@@ -875,6 +924,7 @@ int dp_prepare_pd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
 int dp_prepare_fd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stream) {
   g_err.clear();
   if (!c || !H) return fail(DP_ERR_INVALID, "ctx and H_local must be non-NULL");
+  if (c->cfg.flags & DP_FLAG_FP64) return fail(DP_ERR_UNSUPPORTED, "prepare / apply: not with DP_FLAG_FP64");
   if (!is_device_ptr(H)) return fail(DP_ERR_INVALID, "dp_prepare_fd takes device pointers");
   if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
   if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");
@@ -889,8 +939,7 @@ int dp_prepare_fd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
   a.H = reinterpret_cast<const float2 *>(H);
   a.S = c->S;
   a.nchunks = c->Cl;
-  a.kappa = (float)(k.tau * k.U * N0 / rho_c2);            // Eq. 9
-  a.coef = (float)(k.Es / rho_c2);
+  set_params(a, (k.tau * k.U * N0 / rho_c2), (k.Es / rho_c2));  // Eq. 9
   a.groups = c->Cl;
   a.nbeta = c->Cl;
   a.Gout = c->G;
@@ -907,6 +956,7 @@ int dp_prepare_fd(dp_ctx *c, const dp_c32 *H, double N0, double rho2, void *stre
 int dp_prepare_from_gram(dp_ctx *c, int fd, const dp_c32 *G_packed, double N0, double rho2, void *stream) {
   g_err.clear();
   if (!c || !G_packed) return fail(DP_ERR_INVALID, "ctx and G_packed must be non-NULL");
+  if (c->cfg.flags & DP_FLAG_FP64) return fail(DP_ERR_UNSUPPORTED, "prepare / apply: not with DP_FLAG_FP64");
   if (!is_device_ptr(c, G_packed)) return fail(DP_ERR_INVALID, "dp_prepare_from_gram takes device pointers");
   if (!(N0 >= 0.0) || !std::isfinite(N0)) return fail(DP_ERR_INVALID, "N0 must be finite and >= 0");
   if (!(rho2 > 0.0) || !std::isfinite(rho2)) return fail(DP_ERR_INVALID, "rho2 must be finite and > 0");

@@ -752,6 +752,7 @@ struct Args {
   int pf_dist;          // fd_tc: L2-prefetch the tiles of CTA blockIdx.x + pf_dist (0: off)
   int fold;             // fd_tc: per-subcarrier scalars in-kernel (CTAs per subcarrier; 0 = finish kernel)
   int hrow_off;         // host only: H rows before a.H in its allocation (unequal-cluster runs; TMA extent)
+  double kappa64, coef64;   // DP_FLAG_FP64 kernels (f64.cuh): kappa and coef unrounded
 };
 
 // Programmatic dependent launch: wait for the predecessor grid's completion (and

@@ -1,6 +1,8 @@
 // FFMA vs FFMA2 (fma.rn.f32x2, sm_100a) throughput probe, and a complex-MAC mix:
 // mode 0: 16 independent FFMA chains; mode 1: 16 independent FFMA2 chains (32 FMAs);
-// mode 2: complex MAC acc += conj(o) * v as 2 FFMA2 (broadcast + swapped operand).
+// mode 2: complex MAC acc += conj(o) * v as 2 FFMA2 (broadcast + swapped operand);
+// mode 3: 16 independent DFMA chains (fp64 pipe, the DP_FLAG_FP64 kernels).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 scripts/ffma2_probe.cu -o /tmp/ffma2_probe
 #include <cstdio>
 #include <cuda_runtime.h>
 typedef unsigned long long u64;
@@ -24,6 +26,13 @@ __global__ void k(float *out, int iters, float s) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) fma2(a[i], x[i], y[i]);
     for (int i = 0; i < 16; ++i) r += lo(a[i]);
+  } else if (MODE == 3) {
+    double a[16], x[16], y[16];
+    for (int i = 0; i < 16; ++i) { a[i] = threadIdx.x * 1e-3 + i; x[i] = s + i * 1e-4; y[i] = 1.0 - i * 1e-5; }
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = fma(x[i], y[i], a[i]);
+    for (int i = 0; i < 16; ++i) r += (float)a[i];
   } else {
     u64 a[8], v[8];
     const float ox = s, oy = s * 0.5f;
@@ -43,17 +52,18 @@ __global__ void k(float *out, int iters, float s) {
 int main() {
   float *o; cudaMalloc(&o, 148 * 8 * 1024 * 4);
   int iters = 20000;
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (mode == 0) k<0><<<148 * 8, 256>>>(o, iters, 0.5f);
       if (mode == 1) k<1><<<148 * 8, 256>>>(o, iters, 0.5f);
       if (mode == 2) k<2><<<148 * 8, 256>>>(o, iters, 0.5f);
+      if (mode == 3) k<3><<<148 * 8, 256>>>(o, iters / 4, 0.5f);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b);
-      double fmas = (mode == 0 ? 16.0 : 32.0) * iters * 148.0 * 8 * 256;
-      double instr = 16.0 * iters * 148.0 * 8 * 256 / 32;   // warp instructions
+      double fmas = (mode == 0 ? 16.0 : mode == 3 ? 16.0 / 4 : 32.0) * iters * 148.0 * 8 * 256;
+      double instr = (mode == 3 ? 4.0 : 16.0) * iters * 148.0 * 8 * 256 / 32;   // warp instructions
       if (rep) printf("mode %d: %.1f TFLOP/s  %.2f warp-instr/clk/SM @1.965GHz (%.3f ms)\n", mode, 2 * fmas / ms / 1e9,
                       instr / (ms * 1e-3) / 148 / 1.965e9, ms);
     }
