@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--latency-frames", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time for cpu_baseline")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no JSON extras)")
+    ap.add_argument("--oracle-seconds", action="store_true", help="cpu_baseline leg only: fp64 oracle CPU seconds "
+                    "for BASELINE configs[0] (cfg1) at OMP_NUM_THREADS=1 and at all cores (SURVEY §8(d))")
+    ap.add_argument("--oracle-seconds-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cluster-sizes", default="", help="comma list of C unequal cluster sizes B_c (dp_set_clusters, "
                     "P:157); FD only, power shares B_c / B")
     ap.add_argument("--eager", action="store_true", help="launch the timed steps eagerly (default: replay a CUDA "
@@ -206,6 +209,41 @@ def cpu_baseline(cfg, target_s: float, modes, chunk: int = 96):
     return {"value": bits / el / 1e9, "unit": "Gbit/s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"{reps} x {chunk} subcarriers of {cfg.name} ({'+'.join(m.upper() for m in modes)} frames, "
                       f"fp64 C oracle, OpenMP over subcarriers), {el:.1f} s"}
+
+
+def oracle_seconds_child(reps: int = 5):
+    """One process of --oracle-seconds: cfg1 PD + FD frames through the oracle, median of `reps`."""
+    import oracle
+    from paper_1804_10987_b200 import CONFIGS, synth
+    cfg = CONFIGS[1]
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    f = synth.make_frame(cfg.cfg_id, cfg.n_sc, cfg.B, cfg.U, cfg.K, cfg.M)
+    _oracle_step(cfg, f, N0)
+    ts = {"pd": [], "fd": []}
+    for _ in range(reps):
+        for m in ("pd", "fd"):
+            t = time.perf_counter()
+            _oracle_step(cfg, f, N0, (m,))
+            ts[m].append(time.perf_counter() - t)
+    print(json.dumps({"threads": oracle.num_threads(), **{m: statistics.median(v) for m, v in ts.items()}}))
+
+
+def oracle_seconds():
+    """BASELINE configs[0] ("fp64 oracle (CPU seconds)"): cfg1 frames at 1 thread and at all cores."""
+    out = {"workload": "cfg1: B=16 U=4 C=2 N_sc=64 K=1 QPSK, one PD-WF and one FD-WF frame", "runs": []}
+    for n in (1, os.cpu_count() or 1):
+        env = dict(os.environ, OMP_NUM_THREADS=str(n))
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-seconds-child"], env=env,
+                           capture_output=True, text=True, check=True)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        d["cpu_seconds_frame_pd"], d["cpu_seconds_frame_fd"] = d.pop("pd"), d.pop("fd")
+        out["runs"].append(d)
+    try:
+        out["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except Exception:
+        pass
+    out["nproc"] = os.cpu_count()
+    print(json.dumps(out), flush=True)
 
 
 # ---------------------------------------------------------------- reference arm
@@ -389,6 +427,12 @@ def parity_check(pre, cfg, world, rank, dev, Hs, Ss, modes, N0, nsamp=8):
 # ---------------------------------------------------------------- ours
 def main():
     args = parse()
+    if args.oracle_seconds_child:
+        oracle_seconds_child()
+        return
+    if args.oracle_seconds:
+        oracle_seconds()
+        return
     cfg = get_config(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

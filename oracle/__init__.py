@@ -1,8 +1,8 @@
 """fp64 CPU oracle for the decentralized WF precoders (arXiv 1804.10987).
 
 TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and the
-``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
-package.  The product (``paper_1804_10987_b200``, ``libdp.so``) never imports,
+``cpu_baseline`` / ``--impl reference`` / ``--oracle-seconds`` legs and the N > 1
+sampled parity check of ``bench.py`` may import this package.  The product (``paper_1804_10987_b200``, ``libdp.so``) never imports,
 links or calls it and shares no code with it.
 
 Thin ctypes wrapper around ``oracle.c`` (plain C99 double-complex loops).  The
