@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled oracle check at N > 1")
     ap.add_argument("--latency-frames", type=int, default=200)
+    ap.add_argument("--no-apply", action="store_true", help="skip the prepare/apply per-symbol latency")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time for cpu_baseline")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no JSON extras)")
     ap.add_argument("--oracle-seconds", action="store_true", help="cpu_baseline leg only: fp64 oracle CPU seconds "
@@ -598,6 +599,37 @@ def main():
                   "frames": len(xs), "gbps_at_p50": bits_frame / (p50 / 1e3) / 1e9}
     pre.profile(reset=True)
 
+    # ---------------- prepare / apply: W = A^{-1}/beta cached once per
+    # channel, then one OFDM symbol per dp_apply call (whitening + precode [+ s broadcast]); p50 / p99
+    apply = None
+    if not args.no_apply and not args.fp64 and not sizes:
+        apply = {}
+        s1 = [S[:, :1].contiguous() for S in Ss]
+        x1 = torch.empty((cfg.n_sc, 1, Bl), dtype=torch.complex64, device=dev)
+        for m in modes:
+            prep = pre.prepare_pd if m == "pd" else pre.prepare_fd
+            tp, ta = [], []
+            for i in range(max(20, args.latency_frames // 10)):
+                j = i % R
+                barrier()
+                a, b, c_ = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                a.record(stream)
+                prep(Hs[j], N0, 1.0)
+                b.record(stream)
+                for q in range(10):
+                    pre.apply(Hs[j], s1[(j + q) % R], out=x1)
+                c_.record(stream)
+                torch.cuda.synchronize(dev)
+                tp.append(D.max_over_ranks(a.elapsed_time(b), dev))
+                ta.append(D.max_over_ranks(b.elapsed_time(c_) / 10, dev))
+            tp.sort()
+            ta.sort()
+            apply[m] = {"prepare_ms_p50": tp[len(tp) // 2], "apply_1symbol_ms_p50": ta[len(ta) // 2],
+                        "apply_1symbol_ms_p99": ta[min(len(ta) - 1, int(0.99 * len(ta)))], "samples": len(ta),
+                        "note": "apply = one symbol for all subcarriers (z = W s, x = H^H z), averaged over 10 "
+                                "back-to-back calls per sample; device-timed, max over ranks"}
+        pre.profile(reset=True)
+
     # ---------------- e2e through the C-ABI with pinned HOST buffers (H2D + compute + D2H per call)
     e2e = None
     if not args.no_e2e:
@@ -652,6 +684,7 @@ def main():
                                 "unfused (a)(b)(c)" if args.unfused else "fused single pass"),
                        "launch": launch_mode},
             "modes": lat,
+            "apply": apply,
             "roofline": roof,
             "comm": {"bytes_per_step": 4 * sum(ledger.values()) / args.steps,
                      "by_kind_bytes_per_step": {k: 4 * v / args.steps for k, v in ledger.items()},

@@ -59,8 +59,9 @@ class BerRun:
 
     def point(self, mode: str, C: int, snr_db: float, frames: int, frame0: int = 0, sizes=None, power=None,
               taus=None):
-        """Bit errors and bits for `frames` frames; mode "pd" (= centralized WF), "fd" or
-        "mrt" (fully-distributed MRT, the Fig. 2 baseline).  sizes / power / taus: an unequal
+        """Bit errors and bits for `frames` frames; mode "pd" (= centralized WF), "fd",
+        "mrt" (fully-distributed MRT, the Fig. 2 baseline) or "zf" (centralized zero-forcing, the
+        N0 -> 0 limit of WF: the PD precoder evaluated at N0 = 0, received at the point's N0).  sizes / power / taus: an unequal
         partition for FD / MRT (dp_set_clusters; None = equal split, 1/C, the run's tau)."""
         N0 = 10.0 ** (-snr_db / 10.0)       # rho^2 = Es = 1 (reading R10)
         pre = self._precoder(C)
@@ -69,7 +70,10 @@ class BerRun:
         rx = torch.empty(self.n_sc, dtype=torch.float32, device="cuda")
         for f in range(frame0, frame0 + frames):
             H, s, idx, n = synth_frame(f, self.n_sc, self.B, self.U, self.K, self.M, N0, seed=self.seed)
-            x = {"pd": pre.precode_pd, "fd": pre.precode_fd, "mrt": pre.precode_mrt}[mode](H, s, N0, 1.0)
+            if mode == "zf":
+                x = pre.precode_pd(H, s, 0.0, 1.0)
+            else:
+                x = {"pd": pre.precode_pd, "fd": pre.precode_fd, "mrt": pre.precode_mrt}[mode](H, s, N0, 1.0)
             L.check(L.dp_read_scalars(pre.ctx, L.DP_SCALAR_RX, rx.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream), "dp_read_scalars")
             receive_count(H, x, n, rx, idx, self.M, errors)

@@ -373,12 +373,24 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
   const bool topo_t3 = c->comm_on && k.pd_topology == DP_PD_SCATTER_GATHER;
   const float2 *s_use = sd;
-  if (!topo_t1) RET(distribute_s(c, sd, st, &s_use));   // T2: overlaps nothing yet; only s crosses
+  // s broadcast (allreduce / scatter-gather topologies): issued on the context's side stream so it
+  // overlaps the Gram kernel (s is not needed before the whitening node); joined before the Gram
+  // exchange, so two collectives of the one communicator never run concurrently
+  const bool side = !topo_t1 && c->comm_on && !k.s_on_all_ranks && c->st_side;
+  if (side) {
+    CK(cudaEventRecord(c->ev_side0, st));
+    CK(cudaStreamWaitEvent(c->st_side, c->ev_side0, 0));
+    RET(distribute_s(c, sd, c->st_side, &s_use));
+    CK(cudaEventRecord(c->ev_side1, c->st_side));
+  } else if (!topo_t1) {
+    RET(distribute_s(c, sd, st, &s_use));
+  }
   a.s = s_use;
   // (a) Gram of this rank's antennas: first levels of the adder tree G = sum_c G_c
   const size_t nG = (size_t)k.n_sc * dpk::npacked(k.U) * 2;
   a.Gout = c->G;
   RET(launch_gram_any(c, a, c->pd_nw, false, st));
+  if (side) CK(cudaStreamWaitEvent(st, c->ev_side1, 0));
   a.G = c->G;
   a.zout = c->z;
   if (topo_t3) {
@@ -621,6 +633,12 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
     return rc;
   }
   if (comm_on) {
+    if (cudaStreamCreateWithFlags(&c->st_side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_side0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_side1, cudaEventDisableTiming) != cudaSuccess) {
+      dp_finalize(c);
+      return fail(DP_ERR_CUDA, "side stream / events for the s broadcast");
+    }
     ncclUniqueId id;
     memcpy(&id, k.nccl_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->comm, k.world, id, k.rank);
@@ -812,6 +830,9 @@ int dp_finalize(dp_ctx *c) {
     if (c->ev_join[j]) cudaEventDestroy(c->ev_join[j]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->st_side) cudaStreamDestroy(c->st_side);
+  if (c->ev_side0) cudaEventDestroy(c->ev_side0);
+  if (c->ev_side1) cudaEventDestroy(c->ev_side1);
   void *bufs[] = {c->s_buf, c->G, c->z, c->beta, c->pw, c->fin, c->bad, c->h_dev, c->s_dev, c->x_dev, c->vb, c->rd_buf, c->G64, c->z64};
   for (void *b : bufs)
     if (b) cudaFree(b);

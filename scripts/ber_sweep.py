@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--tau", default="0.125", help="FD regularisation tau_c (Eq. 9); comma list = tau sweep")
     ap.add_argument("--no-pd", action="store_true", help="FD points only")
     ap.add_argument("--mrt", action="store_true", help="add fully-distributed MRT (Fig. 2 baseline) at every C")
+    ap.add_argument("--zf", action="store_true", help="add centralized zero-forcing (WF in the N0 -> 0 limit, P:37)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     lo, hi, step = (float(v) for v in args.snr.split(":"))
@@ -48,10 +49,10 @@ def main():
     t0 = time.time()
     for snr in snrs:
         pts = ([] if args.no_pd else [("pd", 1, taus[0])]) + [("fd", c, t) for t in taus for c in Cs] + \
-              ([("mrt", c, taus[0]) for c in Cs] if args.mrt else [])
+              ([("mrt", c, taus[0]) for c in Cs] if args.mrt else []) + ([("zf", 1, taus[0])] if args.zf else [])
         for mode, C, tau in pts:
             e, bits = runs[tau].point(mode, C, snr, args.frames)
-            row = {"mode": {"pd": "WF(=PD)", "fd": "FD", "mrt": "MRT"}[mode], "C": C, "B": args.B, "U": args.U,
+            row = {"mode": {"pd": "WF(=PD)", "fd": "FD", "mrt": "MRT", "zf": "ZF"}[mode], "C": C, "B": args.B, "U": args.U,
                    "snr_db": snr, "errors": e, "bits": bits, "ber": e / bits, "frames": args.frames}
             if mode == "fd":
                 row["tau"] = tau
