@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="4", help="4 (default), 2, 3 or a paper point fig2a..fig2e")
     ap.add_argument("--K", type=int, default=0, help="override the symbols per frame (e.g. 7 to mirror the paper)")
+    ap.add_argument("--rank-shape", type=int, default=0, help="world-1 run of one rank's shard of the config on N GPUs "
+                    "(B/N antennas, C/N clusters): the per-rank shapes of the scaling curve")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="both", choices=["both", "pd", "fd"])
     ap.add_argument("--unfused", action="store_true", help="three-kernel path (a)(b)(c)")
@@ -77,6 +79,10 @@ def get_config(args):
     if args.K:
         cfg = type(cfg)(cfg.cfg_id, f"{cfg.name}_K{args.K}", cfg.n_sc, cfg.B, cfg.U, cfg.C, args.K, cfg.M,
                         cfg.snr_db, cfg.tau)
+    if args.rank_shape:
+        n = args.rank_shape
+        cfg = type(cfg)(cfg.cfg_id, f"{cfg.name}_rankshape{n}", cfg.n_sc, cfg.B // n, cfg.U, cfg.C // n, cfg.K,
+                        cfg.M, cfg.snr_db, cfg.tau)
     return cfg
 
 
@@ -333,6 +339,15 @@ def roofline(cfg, world, prof, ms_prof, ms_step_unprof, steps, peaks, sizes, fp6
             e.update(bound="alu", flops=f_, achieved_tflops=f_ / (kms / 1e3) / 1e12,
                      frac=f_ / (kms / 1e3) / 1e12 / pipe["tflops"],
                      note="1 U x U problem per subcarrier: latency-bound (SURVEY §8(d): reported, not graded)")
+        elif k == "fused_pd":                        # PD single pass at world 1 (U < 32): all on the FP32 pipe
+            allf = cfg.n_sc * sum(flp.values())
+            b = bf["H"] + bf["s"] + bf["x"]
+            t = kms / 1e3
+            e.update(bound="alu", kernel_path="fd_fused(S=B)", method_flops=allf,
+                     achieved_tflops=allf / t / 1e12, frac=allf / t / 1e12 / pipe["tflops"],
+                     pipes={"simt_steps": ["gram", "solve", "whiten", "precode"], "simt_flops": allf,
+                            "simt_frac": allf / t / 1e12 / pipe["tflops"], "hbm_bytes": b,
+                            "hbm_frac": b / t / 1e9 / hbm})
         elif k == "fused_fd" and not sizes:
             tot, tflops, sflops, tn, sn = fd_pipes(cfg, cfg.U, cfg.S, cfg.K, cfg.n_sc * Cl, fd_path)
             allf = sum(tot.values())

@@ -142,7 +142,9 @@ typedef struct {
 #define DP_KERNEL_SOLVE         2   /* (b) regularise + Cholesky-type sweep + beta + whiten z           */
 #define DP_KERNEL_PRECODE       3   /* (c) x_c = H_c^H z + power partials + per-subcarrier scalars      */
 #define DP_KERNEL_FINISH        4   /* FD per-subcarrier scalar combination                             */
-#define DP_NUM_KERNELS          5
+#define DP_KERNEL_FUSED_PD      5   /* PD single pass at world 1 (U < 32): Gram over all B antennas +
+                                       solve + whiten + precode per subcarrier                          */
+#define DP_NUM_KERNELS          6
 
 /* exchange ledger kinds (dp_comm_ledger index): float payload elements this rank hands to */
 #define DP_COMM_GRAM     0  /* PD: allreduce / reduce of the packed Hermitian Gram     */

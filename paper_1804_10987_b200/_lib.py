@@ -18,7 +18,7 @@ DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST, DP_PD_SCATTER_GATHER = 0, 1, 2
 DP_SCALAR_BETA, DP_SCALAR_RX, DP_SCALAR_POWER = 0, 1, 2
 COMM_KINDS = ["gram", "s_bcast", "z_bcast", "scalars"]   # DP_COMM_* order
 DP_NUM_COMM = len(COMM_KINDS)
-KERNEL_NAMES = ["fused_fd", "gram", "solve", "precode", "finish"]
+KERNEL_NAMES = ["fused_fd", "gram", "solve", "precode", "finish", "fused_pd"]
 DP_NUM_KERNELS = len(KERNEL_NAMES)
 
 # every symbol include/dp.h declares (checked by tests/test_abi.py)

@@ -348,6 +348,20 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   a.groups = 1;
   a.nbeta = 1;
   a.fin_inv_beta = (k.rank == 0) ? 1 : 0;   // 1/beta contributed once to the scalar allreduce
+  if (!c->comm_on && c->pdf_nw > 0 && !(k.flags & (DP_FLAG_UNFUSED | DP_FLAG_FP64))) {
+    // one GPU holds every cluster: the adder tree G = sum_c G_c runs inside the per-subcarrier
+    // Gram accumulation, and the whole PD chain -- Gram over all B antennas, A = G + kappa I, sweep,
+    // Lemma-1 beta, z = A^{-1} s / beta, x_c = H_c^H z for every cluster -- is one single-pass kernel
+    // (fd_fused_kernel with one "cluster" of all B antennas and PD's kappa / coefficient): H is read once
+    a.S = c->Bl;
+    a.nchunks = 1;
+    a.fold = 1;                                           // fin[sc] = {1/beta, power} in-kernel
+    a.s = sd;
+    RET(launch_fd_fused_any(c, a, st, c->pdf_nw, DP_KERNEL_FUSED_PD));
+    c->last_mode = 0;
+    c->prepared = -1;
+    return DP_OK;
+  }
   if (k.flags & DP_FLAG_FP64) {
     // accuracy option (f64.cuh): fp64 partial Gram -> allreduce (ncclDouble) -> fp64 solve and
     // whitening on every rank -> fp64-accumulated local precode
@@ -601,6 +615,21 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   if (smem_fd_fused(k.U, S_fd, k.K, c->fd_nw) > 227 * 1024) {
     delete c;
     return fail(DP_ERR_UNSUPPORTED, "cluster tile S=%d x U=%d does not fit in shared memory", S, k.U);
+  }
+  // single-pass PD at world 1 (fd_fused_kernel with one problem of S = B per sub-group): used for small
+  // problems (B U <= 512, e.g. cfg2: 27.9 -> 25.4 us per frame); for larger U < 32 the per-subcarrier
+  // sub-group is too little parallelism (cfg3: 45.5 -> 50.4 us) and the three-kernel path stays.
+  // DP_PD_FUSED=1 / 0 forces it on (any U < 32) / off.  0: not used
+  c->pdf_nw = 0;
+  {
+    const char *ev = getenv("DP_PD_FUSED");
+    const bool want = ev ? (atoi(ev) != 0) : (c->Bl * k.U <= 512);
+    if (!comm_on && k.U < 32 && want)
+      for (int nw = 4; nw >= 1; nw >>= 1)
+        if (smem_fd_fused(k.U, c->Bl, k.K, nw) <= (nw > 1 ? 100 * 1024 : 227 * 1024)) {
+          c->pdf_nw = nw;
+          break;
+        }
   }
   if (c->pd_nw > 8) {
     delete c;

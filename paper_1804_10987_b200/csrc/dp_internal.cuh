@@ -66,6 +66,7 @@ struct dp_ctx {
   int pd_nw = 0;     // warps per CTA of the per-subcarrier PD kernels
   int fd_nw = 0;     // warps per CTA of the FD fused kernel
   int fdu_nw = 0;    // warps of the FD unfused per-subcarrier kernels (chunk = cluster)
+  int pdf_nw = 0;    // warps per CTA of the single-pass PD kernel at world 1 (0: not used)
   bool comm_on = false;
   bool use_tc = true;        // tensor-core paths where available (env DP_NO_TC=1 disables)
   int num_sms = 148;
@@ -289,7 +290,8 @@ int dispatch(int U, int K, T... args) {
 // Every launcher dispatches on the context's U and the args' K (a.K), counts the launch
 // and brackets it with profiling events (LaunchScope).
 // k_fd.cu: SIMT FD single pass (U <= 32, B_c >= U), MRT, the FD scalar finish kernels
-int launch_fd_fused_any(dp_ctx *c, const Args &a, cudaStream_t st);
+int launch_fd_fused_any(dp_ctx *c, const Args &a, cudaStream_t st, int nw = 0,   // nw 0: c->fd_nw
+                        int kid = DP_KERNEL_FUSED_FD);
 int launch_mrt_u(dp_ctx *c, const Args &a, cudaStream_t st);
 int launch_fd_finish(dp_ctx *c, const Args &a, cudaStream_t st);
 int launch_fd_var_finish(dp_ctx *c, const Args &a, const dpk::VarRuns &vr, cudaStream_t st);

@@ -6,23 +6,25 @@
 namespace dpi {
 
 template <int U, int KC>
-int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st) {
-  const int nw = c->fd_nw;
+int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st, int nw_, int kid) {
+  const int nw = nw_ > 0 ? nw_ : c->fd_nw;
   const int nsg = nw * (32 / U);
   const int nprob = a.n_sc * a.nchunks;
   static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
   const size_t sm = smem_fd_fused(U, a.S, a.K, nw) + pad;
   auto kern = dpk::fd_fused_kernel<U, KC>;
   CK(set_smem(kern, sm));
-  LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
+  LaunchScope ls(c, kid, st);
   CK(launch_pdl(kern, dim3((nprob + nsg - 1) / nsg), dim3(nw * 32), sm, st, a));
   return DP_OK;
 }
 template <int U, int KC> struct FdFused {
-  static int run(dp_ctx *c, const Args &a, cudaStream_t st) { return launch_fd_fused<U, KC>(c, a, st); }
+  static int run(dp_ctx *c, const Args &a, cudaStream_t st, int nw, int kid) {
+    return launch_fd_fused<U, KC>(c, a, st, nw, kid);
+  }
 };
-int launch_fd_fused_any(dp_ctx *c, const Args &a, cudaStream_t st) {
-  return dispatch<FdFused>(c->cfg.U, a.K, c, a, st);
+int launch_fd_fused_any(dp_ctx *c, const Args &a, cudaStream_t st, int nw, int kid) {
+  return dispatch<FdFused>(c->cfg.U, a.K, c, a, st, nw, kid);
 }
 
 template <int U>

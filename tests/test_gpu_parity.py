@@ -586,6 +586,27 @@ def test_profile_and_launch_count():
         # PD: (a) gram, (b) solve, (c) precode ; FD: one fused kernel (each CTA holds whole
         # subcarriers at cfg3, so the per-subcarrier scalars are folded in: no finish kernel)
         assert p["gram"]["launches"] == 1 and p["solve"]["launches"] == 1 and p["precode"]["launches"] == 1
-        assert p["fused_fd"]["launches"] == 1 and p["finish"]["launches"] == 0
+        assert p["fused_fd"]["launches"] == 1 and p["finish"]["launches"] == 0 and p["fused_pd"]["launches"] == 0
         assert p["fused_fd"]["ms"] > 0
         assert pre.launch_count() == 4
+
+
+@pytest.mark.parametrize("unfused", [False, True], ids=["single-pass", "unfused"])
+def test_pd_single_pass_small_world1(unfused):
+    """cfg2 (B U = 512): PD at world 1 is one single-pass kernel (Gram over all B antennas + solve +
+    whitening + precode per subcarrier); DP_FLAG_UNFUSED keeps the three kernels.  Both vs the oracle."""
+    cfg = CONFIGS[2]
+    f = frame(cfg, 70)
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    flags = L.DP_FLAG_PROFILE | (L.DP_FLAG_UNFUSED if unfused else 0)
+    with Precoder(70, cfg.B, cfg.U, cfg.K, cfg.C, flags=flags) as pre:
+        x = pre.precode_pd(torch.from_numpy(f.H).cuda(), torch.from_numpy(f.s).cuda(), N0).cpu().numpy()
+        beta = pre.read_scalars("beta").cpu().numpy()
+        pw = pre.read_scalars("power").cpu().numpy()
+        p = pre.profile(reset=True)
+        assert pre.status() == 0
+    assert (p["fused_pd"]["launches"], p["gram"]["launches"]) == ((0, 1) if unfused else (1, 0))
+    xr, br, _ = reference(cfg, f, "pd", N0)
+    assert rel_l2(x, xr) <= REL_TOL
+    assert np.max(np.abs(beta / br - 1)) <= REL_TOL
+    assert np.max(np.abs(pw / np.sum(np.abs(xr) ** 2, axis=(1, 2)) - 1)) <= 1e-4
