@@ -78,7 +78,7 @@ extern "C" {
 #define DP_ERR_INVALID     2   /* bad argument: NULL pointer, dims, N0 < 0, rho2 <= 0, ...      */
 #define DP_ERR_CUDA        3   /* CUDA runtime error (message in dp_last_error)                 */
 #define DP_ERR_NCCL        4   /* NCCL error                                                    */
-#define DP_ERR_UNSUPPORTED 5   /* e.g. U not in {4,8,16,32}; B/C < U with B/C not in {4,8,16}  */
+#define DP_ERR_UNSUPPORTED 5   /* e.g. U not in {4,8,16,32}; a shape a kernel lacks (dp_last_error)  */
 
 /* dp_config.flags */
 #define DP_FLAG_SYNC        1  /* synchronize at the end of each precode call; return numeric errors */
@@ -114,7 +114,7 @@ typedef struct {
     int U;               /* UEs, 1 <= U <= 32                                                   */
     int K;               /* OFDM symbols per frame sharing one channel, 1..64           */
     int C;               /* antenna clusters, C % world == 0, B % world == 0.  B % C == 0 gives the
-                            equal split B_c = B/C (B/C >= U or in {4, 8, 16}); otherwise FD / MRT
+                            equal split B_c = B/C (any B_c >= 1: B_c < U takes the P:230 branch); otherwise FD / MRT
                             need dp_set_clusters first (unequal B_c)                     */
     int rank, world;     /* this process's rank and the number of GPUs (one process per GPU)    */
     int device;          /* CUDA device ordinal of this rank                                    */
@@ -172,7 +172,7 @@ DP_API int dp_precode_pd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
 /* FD-WF frame (Sec. III-C): for every local cluster c, x_c = Q_c s / beta_c with
  * rho_c^2 = rho2 / C, kappa_c = tau U N0 / rho_c^2 (Eq. 9) and
  *   Q_c = H_c^H (H_c H_c^H + kappa_c I_U)^{-1}        if B_c >= U
- *   Q_c = (H_c^H H_c + kappa_c I_{B_c})^{-1} H_c^H    if B_c <  U (B_c in {4, 8, 16};
+ *   Q_c = (H_c^H H_c + kappa_c I_{B_c})^{-1} H_c^H    if B_c <  U (any 1 <= B_c < U;
  *         defined at N0 = 0 when H_c has full column rank)
  * beta_c^2 = Es tr(Q_c^H Q_c) / rho_c^2.  Only s (and 2 n_sc scalars) cross ranks. */
 DP_API int dp_precode_fd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
@@ -181,7 +181,7 @@ DP_API int dp_precode_fd(dp_ctx *ctx, const dp_c32 *H_local, const dp_c32 *s,
 /* Unequal clusters, per-cluster power and tau ("B_c = w_c B", P:215 with its footnote,
  * Eq. 9 "tau_c").  Host arrays over ALL C clusters (global order), copied:
  *   B_c[C]    cluster sizes, sum = B; each rank's clusters (c in [rank C/world, (rank+1) C/world))
- *             must hold B/world antennas; B_c < U needs B_c in {4, 8, 16} (small-cluster branch);
+ *             must hold B/world antennas; B_c < U takes the small-cluster branch (any size);
  *             NULL = the equal split B/C;
  *   power[C]  shares w_c = rho_c^2 / rho2 > 0 with sum_c w_c = 1 (within 1e-9); NULL = 1/C each;
  *   tau[C]    tau_c >= 0; NULL = cfg.tau for every cluster.

@@ -581,8 +581,6 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   // equal split S = B / C (P:157 with w_c = 1/C); 0 when C does not divide B: the sizes then come
   // from dp_set_clusters before any FD / MRT call
   const int S = (k.B % k.C) ? 0 : k.B / k.C;
-  if (S && S < k.U && S != 4 && S != 8 && S != 16)   // FD branch B_c < U: fd_small.cuh
-    return fail(DP_ERR_UNSUPPORTED, "B/C=%d < U=%d: the small-cluster branch supports B_c in {4, 8, 16}", S, k.U);
   const bool comm_on = k.world > 1 || (k.flags & DP_FLAG_FORCE_COMM);
   if (comm_on && !k.nccl_id) return fail(DP_ERR_INVALID, "nccl_id is required when world > 1 or DP_FLAG_FORCE_COMM");
 
@@ -787,9 +785,6 @@ int dp_set_clusters(dp_ctx *c, const int *B_c, const double *power, const double
     if (sz[i] <= 0) return fail(DP_ERR_INVALID, "B_c[%d]=%d must be positive", i, sz[i]);
     if (!(w[i] > 0.0) || !std::isfinite(w[i])) return fail(DP_ERR_INVALID, "power[%d] must be > 0", i);
     if (!(t[i] >= 0.0) || !std::isfinite(t[i])) return fail(DP_ERR_INVALID, "tau[%d] must be >= 0", i);
-    if (sz[i] < k.U && sz[i] != 4 && sz[i] != 8 && sz[i] != 16)
-      return fail(DP_ERR_UNSUPPORTED, "B_c[%d]=%d < U=%d: the small-cluster branch supports B_c in {4, 8, 16}", i,
-                  sz[i], k.U);
     if (sz[i] >= k.U && !(c->use_tc && k.U == 32 && sz[i] == 32 && k.K <= 16) &&
         smem_fd_fused(k.U, sz[i], k.K, c->fd_nw) > 227 * 1024)
       return fail(DP_ERR_UNSUPPORTED, "B_c[%d]=%d: the FD tile needs more than 227 KB of shared memory", i, sz[i]);

@@ -409,7 +409,7 @@ __device__ __forceinline__ float solve_sg(float2 (&a)[U], float2 (&d)[U], float2
 // HPD) or beta's radicand is not.  slot: 2U complex.
 template <int U>
 __device__ __forceinline__ float sweep_sg(float2 (&w)[U], float2 *slot, int l, float kappa, float coef,
-                                          bool &ok) {
+                                          bool &ok, int nvalid = U) {
   constexpr int R = U >= 4 ? 4 : U;
   ok = true;
   // ---- Jacobi equilibration A' = D^{-1/2} A D^{-1/2} (unit diagonal, pivots in (0, 1])
@@ -499,6 +499,7 @@ __device__ __forceinline__ float sweep_sg(float2 (&w)[U], float2 *slot, int l, f
     if (p + 1 == l) tr = -w[p + 1].x;
   }
   __syncwarp();
+  if (l >= nvalid) tr = f = 0.f;                  // padding lanes (fd_small.cuh): decoupled unit block
   tr = sg_sum<U>(tr);
   f = sg_sum<U>(f);
   // Lemma 1, Eq. (6):  beta^2 = Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)

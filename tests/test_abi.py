@@ -73,7 +73,7 @@ def _cfg(**kw):
     (dict(pd_topology=7), L.DP_ERR_INVALID),
     (dict(world=2), L.DP_ERR_INVALID),          # world > 1 needs nccl_id
     (dict(U=5), L.DP_ERR_UNSUPPORTED),
-    (dict(U=16, B=24, C=4), L.DP_ERR_UNSUPPORTED),   # B/C = 6 < U: small-cluster branch needs B_c in {4, 8, 16}
+    (dict(U=64, B=128, C=2), L.DP_ERR_UNSUPPORTED),  # U > 32
 ])
 def test_dp_init_rejects_bad_config(kw, code):
     ctx = ctypes.c_void_p()

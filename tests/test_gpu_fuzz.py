@@ -22,7 +22,7 @@ def _case(seed: int):
     rng = np.random.default_rng(1000 + seed)
     U = int(rng.choice([4, 8, 16, 32]))
     C = int(rng.choice([1, 2, 4, 8]))
-    sizes = [U, 2 * U, 4 * U] + [b for b in (4, 8, 16) if b < U]
+    sizes = [U, 2 * U, 4 * U] + [b for b in (2, 4, 6, 8, 16, 24) if b < U]
     S = int(rng.choice(sizes))
     if S * C > 256:
         C = max(1, 256 // S)
@@ -59,7 +59,7 @@ def _var_case(seed: int):
     per-cluster tau_c; C need not divide B."""
     rng = np.random.default_rng(5000 + seed)
     U = int(rng.choice([4, 8, 16, 32]))
-    allowed = [U, U + 8, 2 * U, 3 * U] + [b for b in (4, 8, 16) if b < U]
+    allowed = [U, U + 8, 2 * U, 3 * U] + [b for b in (3, 4, 8, 12, 16, 20) if b < U]
     C = int(rng.integers(2, 9))
     sizes = [int(rng.choice(allowed)) for _ in range(C)]
     if rng.random() < 0.5:                            # long runs of equal clusters too

@@ -392,6 +392,25 @@ def test_small_clusters_bc_below_u(S, U, mode):
     assert np.max(np.abs(pw / pwr - 1)) <= 1e-4
 
 
+@pytest.mark.parametrize("S,U", [(1, 4), (3, 4), (5, 8), (6, 8), (10, 16), (12, 16), (20, 32), (24, 32), (31, 32)])
+@pytest.mark.parametrize("N0", [0.1, 0.0], ids=["10dB", "N0=0"])
+def test_small_clusters_any_size(S, U, N0):
+    """B_c < U of any size (not a power of two): the sub-group is padded to the next power of two with
+    zero antenna rows and a unit diagonal (a decoupled block, left out of beta's traces); x, beta_c,
+    the receive scale and the power vs the oracle's B_c x B_c branch, also in the ZF limit."""
+    base = CONFIGS[3]
+    C = 3
+    cfg = type(base)(base.cfg_id, f"s{S}u{U}", 19, S * C, U, C, 14, 16)
+    f = frame(cfg)
+    x, beta, rx, pw, nbad = run(cfg, f, "fd", N0)
+    xr, br, rxr = reference(cfg, f, "fd", N0)
+    assert nbad == 0
+    assert rel_l2(x, xr) <= REL_TOL, rel_l2(x, xr)
+    assert np.max(np.abs(beta.reshape(br.shape) / br - 1)) <= REL_TOL
+    assert np.max(np.abs(rx / rxr - 1)) <= REL_TOL
+    assert np.max(np.abs(pw / np.sum(np.abs(xr) ** 2, axis=(1, 2)) - 1)) <= 1e-4
+
+
 def test_small_clusters_zero_noise():
     """At N0 = 0 the B_c x B_c branch stays defined (H_c^H H_c has full rank B_c < U) where
     the U x U form would be singular: FD precodes without numeric failures and matches the

@@ -121,9 +121,10 @@ def test_set_clusters_errors():
         with pytest.raises(L.DpError) as e:
             pre.set_clusters([32, 32, 32, 16])                      # sum 112 != 128
         assert e.value.code == L.DP_ERR_INVALID
+        pre.set_clusters([6, 26, 48, 48])                           # any B_c >= 1 (B_c < U: padded sub-group)
         with pytest.raises(L.DpError) as e:
-            pre.set_clusters([6, 26, 48, 48])                       # B_c = 6 < U not a supported size
-        assert e.value.code == L.DP_ERR_UNSUPPORTED
+            pre.set_clusters([0, 32, 48, 48])                       # B_c = 0
+        assert e.value.code == L.DP_ERR_INVALID
         with pytest.raises(L.DpError) as e:
             pre.set_clusters(None, [0.5, 0.5, 0.5, 0.5])            # shares sum to 2
         assert e.value.code == L.DP_ERR_INVALID
