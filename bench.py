@@ -499,7 +499,7 @@ def main():
     # ---------------- resident rotating input sets (> 2x L2 in total)
     bf = bytes_frame(cfg, Bl)
     per_set = bf["H"] + bf["s"] + bf["x"]
-    R = max(2, math.ceil(2 * L2_BYTES / per_set))
+    R = max(3, math.ceil(2 * L2_BYTES / per_set))
     gen = torch.Generator(device=dev)
     gen.manual_seed(SEED + 1000 * cfg.cfg_id + rank)
     pts = torch.from_numpy(synth.QAM(cfg.M).points().astype("complex64")).to(dev)
@@ -515,9 +515,11 @@ def main():
     modes = ["pd", "fd"] if args.mode == "both" else [args.mode]
 
     def step(i, p=None):
+        # each frame of the step gets its own input set (the PD and the FD frame of a step never
+        # share H, so FD cannot read the H that PD just pulled into L2)
         p = p or pre
-        j = i % R
-        for m in modes:
+        for q, m in enumerate(modes):
+            j = (len(modes) * i + q) % R
             fn = p.precode_pd if m == "pd" else p.precode_fd
             fn(Hs[j], Ss[j], N0, 1.0, out=Xs[j])
 
