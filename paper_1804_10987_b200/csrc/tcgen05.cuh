@@ -98,6 +98,24 @@ __device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count));
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+#ifdef DP_HANG_DEBUG
+// diagnostics builds only: a wait that spins ~2^27 polls reports the barrier and traps
+__device__ __noinline__ void mbar_wait_dbg(uint64_t *mbar, uint32_t phase, int line) {
+  uint32_t ok = 0;
+  for (long long it = 0; !ok; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(mbar)), "r"(phase)
+        : "memory");
+    if (!ok && it == (1ll << 27)) {
+      printf("HANG block %d thread %d line %d bar %p phase %u\n", blockIdx.x, threadIdx.x, line, mbar, phase);
+      asm volatile("trap;");
+    }
+  }
+}
+#define mbar_wait(m, p) mbar_wait_dbg(m, p, __LINE__)
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
@@ -107,6 +125,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+#endif
 
 // wait with exponential nanosleep back-off (single-thread producer / issuer roles, so a
 // spinning thread does not steal issue slots from the working warps)

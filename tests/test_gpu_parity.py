@@ -610,6 +610,36 @@ def test_profile_and_launch_count():
         assert pre.launch_count() == 4
 
 
+def test_consecutive_frames_cfg4():
+    """cfg4 (U = B_c = 32, C = 8): several consecutive PD and FD frames on one context, launched
+    back to back (PDL lets each kernel start while its predecessor drains, so mbarrier-phase or
+    hand-off hazards that a single synchronised frame hides show up here), 600 subcarriers so the
+    persistent PD kernels loop over several items per CTA; every frame against the oracle, and
+    the FD scalars folded into the tensor-core kernel (no finish kernel)."""
+    cfg = CONFIGS[4]
+    n_sc = 600
+    f = frame(cfg, n_sc)
+    N0 = synth.n0_from_snr_db(cfg.snr_db)
+    with Precoder(n_sc, cfg.B, cfg.U, cfg.K, cfg.C, tau=cfg.tau, flags=L.DP_FLAG_PROFILE) as pre:
+        H = torch.from_numpy(f.H).cuda()
+        s = torch.from_numpy(f.s).cuda()
+        for mode in ("pd", "fd", "pd", "fd", "fd"):
+            x = (pre.precode_pd if mode == "pd" else pre.precode_fd)(H, s, N0, 1.0).cpu().numpy()
+            beta = pre.read_scalars("beta").cpu().numpy()
+            rx = pre.read_scalars("rx").cpu().numpy()
+            pw = pre.read_scalars("power").cpu().numpy()
+            xr, br, rxr = reference(cfg, f, mode, N0)
+            assert rel_l2(x, xr) <= REL_TOL, (mode, rel_l2(x, xr))
+            assert np.max(np.abs(beta.reshape(br.shape) / br - 1)) <= REL_TOL
+            assert np.max(np.abs(rx / rxr - 1)) <= REL_TOL
+            pwr = np.sum(np.abs(xr) ** 2, axis=(1, 2))
+            assert np.max(np.abs(pw / pwr - 1)) <= 1e-4
+        p = pre.profile(reset=True)
+        assert pre.status() == 0
+    assert p["fused_fd"]["launches"] == 3 and p["finish"]["launches"] == 0
+    assert p["solve"]["launches"] == 2 and p["precode"]["launches"] == 2
+
+
 @pytest.mark.parametrize("unfused", [False, True], ids=["single-pass", "unfused"])
 def test_pd_single_pass_small_world1(unfused):
     """cfg2 (B U = 512): PD at world 1 is one single-pass kernel (Gram over all B antennas + solve +
