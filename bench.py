@@ -54,8 +54,11 @@ def parse():
     ap.add_argument("--mode", default="both", choices=["both", "pd", "fd"])
     ap.add_argument("--unfused", action="store_true", help="three-kernel path (a)(b)(c)")
     ap.add_argument("--fp64", action="store_true", help="DP_FLAG_FP64 accuracy option (fp64 accumulation)")
-    ap.add_argument("--pd-topology", default="scatter_gather", choices=["allreduce", "reduce_bcast", "scatter_gather"],
-                    help="PD exchange for N > 1 (DESIGN.md §6); scatter_gather splits the solve over the GPUs")
+    ap.add_argument("--pd-topology", default="scatter_gather", choices=["allreduce", "reduce_bcast", "scatter_gather", "nvlink"],
+                    help="PD exchange for N > 1 (DESIGN.md §6); scatter_gather splits the solve over the GPUs, nvlink "
+                    "does the same with the exchange inside the whitening kernel (NVLink load/store, U = 32)")
+    ap.add_argument("--force-comm", action="store_true", help="world 1: run the exchange path on a 1-rank NCCL "
+                    "communicator (DP_FLAG_FORCE_COMM), e.g. to time --pd-topology nvlink against scatter_gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled oracle check at N > 1")
@@ -481,9 +484,11 @@ def main():
     # (DP_FLAG_PROFILE: CUDA events around every kernel, on the launching stream) runs the
     # same steps right after it for the per-kernel times of the roofline.
     flags = (L.DP_FLAG_UNFUSED if args.unfused else 0) | (L.DP_FLAG_FP64 if args.fp64 else 0)
+    force = world == 1 and args.force_comm
+    flags |= L.DP_FLAG_FORCE_COMM if force else 0
     mk = lambda fl: Precoder(cfg.n_sc, cfg.B, cfg.U, cfg.K, cfg.C, rank=rank, world=world, device=local,  # noqa: E731
                              tau=cfg.tau, pd_topology=args.pd_topology, s_on_all_ranks=(world == 1), flags=fl,
-                             nccl_id=D.bootstrap_nccl_id() if world > 1 else None)
+                             nccl_id=D.bootstrap_nccl_id() if world > 1 else (L.dp_get_unique_id() if force else None))
     pre = mk(flags)
     pre_prof = mk(flags | L.DP_FLAG_PROFILE)
 

@@ -104,6 +104,14 @@ extern "C" {
                                   and whitens, broadcast z                                             */
 #define DP_PD_SCATTER_GATHER 2 /* reduce-scatter G over subcarrier blocks, each rank solves and whitens
                                   its n_sc/world subcarriers, all-gather z and beta (n_sc % world == 0)  */
+#define DP_PD_NVLINK        3  /* DP_PD_SCATTER_GATHER's split with the exchange inside the whitening
+                                  kernel: each rank sums its subcarriers' partial Grams straight from
+                                  every peer's memory and stores z and beta into every peer's memory
+                                  over NVLink load/store, with per-CTA cross-GPU barriers (NCCL 2.28
+                                  device API: symmetric windows, LSA pointers and barriers; DESIGN.md
+                                  §6).  U = 32, n_sc % world == 0, every rank load/store-accessible
+                                  (dp_init: DP_ERR_UNSUPPORTED otherwise).  G, z and beta are then
+                                  ncclMemAlloc'd symmetric windows                                    */
 
 typedef struct { float re, im; } dp_c32;
 typedef struct dp_ctx dp_ctx;                       /* opaque */
@@ -122,7 +130,7 @@ typedef struct {
                             all ranks; NULL iff world == 1 (without DP_FLAG_FORCE_COMM)         */
     double Es;           /* average symbol energy of the constellation (reading R1), > 0 */
     double tau;          /* FD regularisation scale tau_c (Eq. 9; P:241 default 0.125), >= 0    */
-    int pd_topology;     /* DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST or DP_PD_SCATTER_GATHER          */
+    int pd_topology;     /* DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST, DP_PD_SCATTER_GATHER or DP_PD_NVLINK */
     int s_on_all_ranks;  /* 1: s is valid on every rank; 0: s is read on rank 0 only and
                             broadcast by the library ("s is the only signal that must be
                             broadcast")                                    */

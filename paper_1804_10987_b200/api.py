@@ -40,7 +40,8 @@ class Precoder:
                          nccl_id=ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf is not None else None,
                          Es=Es, tau=tau,
                          pd_topology={"allreduce": L.DP_PD_ALLREDUCE, "reduce_bcast": L.DP_PD_REDUCE_BCAST,
-                                      "scatter_gather": L.DP_PD_SCATTER_GATHER}[pd_topology],
+                                      "scatter_gather": L.DP_PD_SCATTER_GATHER,
+                                      "nvlink": L.DP_PD_NVLINK}[pd_topology],
                          s_on_all_ranks=int(s_on_all_ranks), flags=flags)
         self.cfg = cfg
         self.ctx = L.dp_init(cfg)

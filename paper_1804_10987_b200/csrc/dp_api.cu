@@ -386,6 +386,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   }
   const bool topo_t1 = c->comm_on && k.pd_topology == DP_PD_REDUCE_BCAST;
   const bool topo_t3 = c->comm_on && k.pd_topology == DP_PD_SCATTER_GATHER;
+  const bool topo_nvl = c->comm_on && k.pd_topology == DP_PD_NVLINK && c->lsa && !(k.flags & DP_FLAG_FP64);
   const float2 *s_use = sd;
   // s broadcast (allreduce / scatter-gather topologies): issued on the context's side stream so it
   // overlaps the Gram kernel (s is not needed before the whitening node); joined before the Gram
@@ -407,7 +408,20 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   if (side) CK(cudaStreamWaitEvent(st, c->ev_side1, 0));
   a.G = c->G;
   a.zout = c->z;
-  if (topo_t3) {
+  if (topo_nvl) {
+    // subcarrier-split whitening node with the exchange inside the kernel (exch_lsa.cuh): rank r sums
+    // its block's partial Grams straight from the peers' windows, solves, and stores z and beta into
+    // every peer's window -- the reduce-scatter and the all-gather of DP_PD_SCATTER_GATHER without a
+    // collective between kernels
+    const int nb = k.n_sc / k.world, sc0 = k.rank * nb;
+    Args b = a;
+    b.n_sc = nb;
+    b.zout = c->z + (size_t)sc0 * k.K * k.U;
+    b.beta = c->beta + sc0;
+    RET(launch_solve_lsa(c, b, sc0, st));
+    LEDGER(c, DP_COMM_GRAM, nG);                          // the same payload the collectives would move
+    LEDGER(c, DP_COMM_Z_BCAST, (size_t)nb * k.K * k.U * 2 + (size_t)nb);
+  } else if (topo_t3) {
     // subcarrier-split whitening node: rank r receives sum_c G_c of its n_sc/world subcarriers
     // (reduce-scatter, in place), solves and whitens them, and the z / beta blocks are
     // all-gathered: the solve scales with the GPU count instead of running on every rank
@@ -437,7 +451,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
     LEDGER(c, DP_COMM_GRAM, nG);
   }
   // (b) whitening node: A = G + kappa I, LDL^H, A^{-1}, beta (Lemma 1), z = A^{-1} s / beta
-  if (!topo_t3 && (!topo_t1 || k.rank == 0)) RET(launch_solve_any(c, a, st));
+  if (!topo_t3 && !topo_nvl && (!topo_t1 || k.rank == 0)) RET(launch_solve_any(c, a, st));
   if (topo_t1) {
     // master broadcasts z and beta
     NK(ncclGroupStart());
@@ -572,10 +586,13 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
   if (k.C % k.world) return fail(DP_ERR_INVALID, "C=%d not divisible by world=%d", k.C, k.world);
   if (!(k.Es > 0.0) || !std::isfinite(k.Es)) return fail(DP_ERR_INVALID, "Es must be > 0");
   if (!(k.tau >= 0.0) || !std::isfinite(k.tau)) return fail(DP_ERR_INVALID, "tau must be >= 0");
-  if (k.pd_topology != DP_PD_ALLREDUCE && k.pd_topology != DP_PD_REDUCE_BCAST && k.pd_topology != DP_PD_SCATTER_GATHER)
+  if (k.pd_topology != DP_PD_ALLREDUCE && k.pd_topology != DP_PD_REDUCE_BCAST && k.pd_topology != DP_PD_SCATTER_GATHER &&
+      k.pd_topology != DP_PD_NVLINK)
     return fail(DP_ERR_INVALID, "pd_topology %d", k.pd_topology);
-  if (k.pd_topology == DP_PD_SCATTER_GATHER && k.n_sc % k.world)
-    return fail(DP_ERR_INVALID, "DP_PD_SCATTER_GATHER needs n_sc=%d divisible by world=%d", k.n_sc, k.world);
+  if ((k.pd_topology == DP_PD_SCATTER_GATHER || k.pd_topology == DP_PD_NVLINK) && k.n_sc % k.world)
+    return fail(DP_ERR_INVALID, "pd_topology %d needs n_sc=%d divisible by world=%d", k.pd_topology, k.n_sc, k.world);
+  if (k.pd_topology == DP_PD_NVLINK && k.U != 32)
+    return fail(DP_ERR_UNSUPPORTED, "DP_PD_NVLINK: U=%d (the fused-exchange whitening kernel is U = 32)", k.U);
   if (k.U != 4 && k.U != 8 && k.U != 16 && k.U != 32)
     return fail(DP_ERR_UNSUPPORTED, "U=%d: supported U are 4, 8, 16, 32", k.U);
   // equal split S = B / C (P:157 with w_c = 1/C); 0 when C does not divide B: the sizes then come
@@ -641,9 +658,12 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
     if (rc == DP_OK) rc = alloc(p, b);
   };
   if (comm_on && !k.s_on_all_ranks) A((void **)&c->s_buf, n_sc * k.K * k.U * 8);
-  A((void **)&c->G, n_sc * groups * NP * 8);
-  A((void **)&c->z, n_sc * groups * k.K * k.U * 8);
-  A((void **)&c->beta, n_sc * groups * 4);
+  const bool nvl = comm_on && k.pd_topology == DP_PD_NVLINK;   // G, z, beta: symmetric windows (lsa_setup)
+  if (!nvl) {
+    A((void **)&c->G, n_sc * groups * NP * 8);
+    A((void **)&c->z, n_sc * groups * k.K * k.U * 8);
+    A((void **)&c->beta, n_sc * groups * 4);
+  }
   c->pw_len = n_sc * std::max<size_t>(std::max(c->pd_nchunks, c->Cl), 1);
   A((void **)&c->pw, c->pw_len * 4);
   A((void **)&c->fin, n_sc * 2 * 4);
@@ -672,6 +692,15 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
     if (r != ncclSuccess) {
       dp_finalize(c);
       return fail(DP_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    if (k.pd_topology == DP_PD_NVLINK) {
+      const int rl = lsa_setup(c);
+      if (rl != DP_OK) {
+        std::string e = g_err;
+        dp_finalize(c);
+        g_err = e;
+        return rl;
+      }
     }
   }
   *out = c;
@@ -846,6 +875,7 @@ int dp_finalize(dp_ctx *c) {
   cudaDeviceSynchronize();
   drain_profile(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm && (c->lsa || c->devcomm || c->win_g || c->win_z || c->win_b)) lsa_teardown(c);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->st_h2d) cudaStreamDestroy(c->st_h2d);
   if (c->st_d2h) cudaStreamDestroy(c->st_d2h);

@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 #include <cmath>
@@ -112,6 +113,10 @@ struct dp_ctx {
   double prof_ms[DP_NUM_KERNELS] = {0};
   long long prof_n[DP_NUM_KERNELS] = {0};
   long long launches = 0;
+  // DP_PD_NVLINK (k_lsa.cu): symmetric windows over G, z, beta (ncclMemAlloc'd) and the device communicator
+  ncclWindow_t win_g = nullptr, win_z = nullptr, win_b = nullptr;
+  ncclDevComm *devcomm = nullptr;
+  bool lsa = false;
   // exchange ledger: float payload elements handed to each kind of collective by this rank
   long long ledger[DP_NUM_COMM] = {0};
 };
@@ -307,6 +312,9 @@ int launch_whiten_any(dp_ctx *c, const Args &a, cudaStream_t st);
 // k_tc.cu: tensor-core kernels (tcgen05 / TMEM / TMA)
 int launch_gram_tc2_any(dp_ctx *c, const Args &b, cudaStream_t st);   // b.S % 32 == 0, U in {16, 32}
 bool precode_tc2_ok(const dp_ctx *c, const Args &a);
+int lsa_setup(dp_ctx *c);
+void lsa_teardown(dp_ctx *c);
+int launch_solve_lsa(dp_ctx *c, const Args &a, int sc0, cudaStream_t st);
 int launch_precode_tc2(dp_ctx *c, const Args &a, cudaStream_t st);
 bool fd_tc_ok(const dp_ctx *c, const Args &a);
 int fd_fold_of(const dp_ctx *c, const Args &a);

@@ -55,7 +55,7 @@ def library_payload(world: int, n_sc: int, K: int, U: int, mode: str, topology: 
     out["gram"] = n_sc * U * (U + 1) // 2 * 2
     if topology == "reduce_bcast":
         out["z_bcast"] = s_floats + n_sc        # z and beta from rank 0
-    elif topology == "scatter_gather":
+    elif topology in ("scatter_gather", "nvlink"):   # nvlink: the same payload, moved by the solve kernel
         out["s_bcast"] = 0 if s_on_all_ranks else s_floats
         out["z_bcast"] = (n_sc // world) * K * U * 2 + n_sc // world   # this rank's z / beta block
     else:

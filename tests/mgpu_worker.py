@@ -50,7 +50,7 @@ def main():
     def gather(x):
         return D.gather_antennas(x).cpu().numpy()
 
-    for topo in ("allreduce", "reduce_bcast", "scatter_gather"):
+    for topo in ("allreduce", "reduce_bcast", "scatter_gather") + (("nvlink",) if cfg.U == 32 else ()):
         with Precoder(n_sc, cfg.B, cfg.U, cfg.K, cfg.C, rank=rank, world=world, device=local, tau=cfg.tau,
                       pd_topology=topo, s_on_all_ranks=False, nccl_id=D.bootstrap_nccl_id()) as pre:
             x = pre.precode_pd(Hl, s if rank == 0 else None, N0, 1.0)

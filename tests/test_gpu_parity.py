@@ -526,7 +526,9 @@ def test_fd_single_cluster_tau1_equals_pd():
 @pytest.mark.parametrize("cfgid", [3, 4])
 def test_force_comm_world1_paths(cfgid):
     """NCCL code path with a 1-rank communicator: PD allreduce topology, PD paper
-    topology (reduce + z broadcast) and FD (s broadcast + scalar allreduce)."""
+    topology (reduce + z broadcast), the subcarrier split with collectives and (U = 32) with
+    the exchange inside the whitening kernel (NCCL device API: symmetric windows, LSA loads /
+    stores and per-CTA barriers on a 1-rank team), and FD (s broadcast + scalar allreduce)."""
     cfg = CONFIGS[cfgid]
     f = frame(cfg, 31)
     N0 = 0.1
@@ -534,14 +536,53 @@ def test_force_comm_world1_paths(cfgid):
     xr_pd, *_ = reference(cfg, f, "pd", N0)
     xr_fd, *_ = reference(cfg, f, "fd", N0)
     x_fd_plain, *_ = run(cfg, f, "fd", N0)
-    for topo in ("allreduce", "reduce_bcast", "scatter_gather"):
+    topos = ("allreduce", "reduce_bcast", "scatter_gather") + (("nvlink",) if cfg.U == 32 else ())
+    for topo in topos:
         x, beta, rx, pw, nbad = run(cfg, f, "pd", N0, flags=L.DP_FLAG_FORCE_COMM, nccl_id=uid,
                                     pd_topology=topo, s_on_all_ranks=False)
-        assert nbad == 0 and rel_l2(x, xr_pd) <= REL_TOL
+        assert nbad == 0 and rel_l2(x, xr_pd) <= REL_TOL, (topo, rel_l2(x, xr_pd))
         uid = L.dp_get_unique_id()
     x, *_ = run(cfg, f, "fd", N0, flags=L.DP_FLAG_FORCE_COMM, nccl_id=uid, s_on_all_ranks=False)
     assert np.array_equal(x, x_fd_plain)   # same kernels, same order: bit-exact
     assert rel_l2(x, xr_fd) <= REL_TOL
+
+
+def test_nvlink_exchange_world1_consecutive_frames():
+    """DP_PD_NVLINK on a 1-rank communicator over consecutive frames (the per-CTA LSA barriers
+    carry their epochs from launch to launch; the windows are rewritten every frame), with FD
+    frames in between and a CUDA-graph capture of two PD frames; every PD frame against the
+    oracle, and bit-identical to the scatter-gather topology's collectives (same Gram, same
+    summation, same solve kernel arithmetic)."""
+    cfg = CONFIGS[4]
+    n_sc = 96
+    N0 = 0.1
+    frames = [frame(cfg, n_sc, frame_id=i) for i in range(3)]
+    refs = [reference(cfg, f, "pd", N0)[0] for f in frames]
+    outs = {}
+    for topo in ("scatter_gather", "nvlink"):
+        uid = L.dp_get_unique_id()
+        with Precoder(n_sc, cfg.B, cfg.U, cfg.K, cfg.C, flags=L.DP_FLAG_FORCE_COMM, nccl_id=uid,
+                      pd_topology=topo, s_on_all_ranks=True) as pre:
+            Hs = [torch.from_numpy(f.H).cuda() for f in frames]
+            Ss = [torch.from_numpy(f.s).cuda() for f in frames]
+            xs = []
+            for i in range(3):
+                xs.append(pre.precode_pd(Hs[i], Ss[i], N0, 1.0).cpu().numpy())
+                pre.precode_fd(Hs[i], Ss[i], N0, 1.0)
+            X = [torch.empty((n_sc, cfg.K, cfg.B), dtype=torch.complex64, device="cuda") for _ in range(2)]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                pre.precode_pd(Hs[1], Ss[1], N0, 1.0, out=X[0])
+                pre.precode_pd(Hs[2], Ss[2], N0, 1.0, out=X[1])
+            g.replay()
+            torch.cuda.synchronize()
+            xs += [X[0].cpu().numpy(), X[1].cpu().numpy()]
+            assert pre.status() == 0
+        outs[topo] = xs
+        for x, xr in zip(xs, refs + refs[1:]):
+            assert rel_l2(x, xr) <= REL_TOL, (topo, rel_l2(x, xr))
+    for a, b in zip(outs["scatter_gather"], outs["nvlink"]):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("cfgid", [1, 3, 4])

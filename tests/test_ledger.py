@@ -38,7 +38,7 @@ def test_library_payload_forms():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode,topology", [("pd", "allreduce"), ("pd", "reduce_bcast"), ("pd", "scatter_gather"),
-                                           ("fd", "allreduce")])
+                                           ("pd", "nvlink"), ("fd", "allreduce")])
 def test_library_counters_match(mode, topology):
     import torch
 
@@ -46,7 +46,7 @@ def test_library_counters_match(mode, topology):
     from paper_1804_10987_b200 import _lib as L
     from paper_1804_10987_b200 import dist as D
     from paper_1804_10987_b200.api import Precoder
-    cfg = CONFIGS[3]
+    cfg = CONFIGS[4] if topology == "nvlink" else CONFIGS[3]   # the fused-exchange kernel is U = 32
     n_sc = 11
     f = synth.make_frame(cfg.cfg_id, n_sc, cfg.B, cfg.U, cfg.K, cfg.M)
     uid = L.dp_get_unique_id()
