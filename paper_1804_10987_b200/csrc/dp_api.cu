@@ -284,7 +284,8 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
     const bool tc = fd_tc_ok(c, a);
     // SIMT kernel: fold the scalars when every CTA holds whole subcarriers
     const int nsg = c->fd_nw * (32 / k.U);
-    const bool simt_fold = !tc && nsg <= 32 && nsg % c->Cl == 0 && getenv("DP_NO_FOLD") == nullptr;
+    const int npb = nsg / fd_rep(c, a, c->fd_nw);          // problems per CTA of the SIMT kernel
+    const bool simt_fold = !tc && npb <= 32 && npb % c->Cl == 0 && getenv("DP_NO_FOLD") == nullptr;
     if (tc) RET(launch_fd_tc_kc(c, a, st));
     else {
       a.fold = simt_fold ? 1 : 0;
@@ -631,14 +632,15 @@ int dp_init(const dp_config *cfg, dp_ctx **out) {
     delete c;
     return fail(DP_ERR_UNSUPPORTED, "cluster tile S=%d x U=%d does not fit in shared memory", S, k.U);
   }
-  // single-pass PD at world 1 (fd_fused_kernel with one problem of S = B per sub-group): used for small
-  // problems (B U <= 512, e.g. cfg2: 27.9 -> 25.4 us per frame); for larger U < 32 the per-subcarrier
-  // sub-group is too little parallelism (cfg3: 45.5 -> 50.4 us) and the three-kernel path stays.
+  // single-pass PD at world 1 (fd_fused_kernel with one problem of S = B per subcarrier, its rows split
+  // over up to 32/U sub-groups, fd_rep): used for B U <= 1024 (cfg2; Fig. 2(d) B = 64, U = 16: 17.8 ->
+  // 15.7 us per frame, p50 33.5 -> 26.8 us); at cfg3 (B U = 2048) it is 31.5 vs ~29 us per frame
+  // and the three-kernel path stays.
   // DP_PD_FUSED=1 / 0 forces it on (any U < 32) / off.  0: not used
   c->pdf_nw = 0;
   {
     const char *ev = getenv("DP_PD_FUSED");
-    const bool want = ev ? (atoi(ev) != 0) : (c->Bl * k.U <= 512);
+    const bool want = ev ? (atoi(ev) != 0) : (c->Bl * k.U <= 1024);
     if (!comm_on && k.U < 32 && want)
       for (int nw = 4; nw >= 1; nw >>= 1)
         if (smem_fd_fused(k.U, c->Bl, k.K, nw) <= (nw > 1 ? 100 * 1024 : 227 * 1024)) {

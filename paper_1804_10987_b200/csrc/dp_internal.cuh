@@ -171,9 +171,10 @@ inline int solve_scr_u(int U, int K) {
 }
 
 // ---------------------------------------------------------------- smem sizes (bytes)
-inline size_t smem_fd_fused(int U, int S, int K, int nw) {
-  const int PPW = 32 / U;
-  return (size_t)nw * PPW * (S * U + fd_scr_u(U, K)) * sizeof(float2);
+// fd_fused_kernel: per problem [tile S x U][rep scratch]; nw warps of 32 / U sub-groups
+inline size_t smem_fd_fused(int U, int S, int K, int nw, int rep = 1) {
+  const int nsg = nw * (32 / U);
+  return ((size_t)(nsg / rep) * S * U + (size_t)nsg * fd_scr_u(U, K)) * sizeof(float2);
 }
 inline size_t smem_gram(int U, int Bl, int nw) {
   return ((size_t)Bl * U + (size_t)(nw / 2) * 32 * (U / 2 + U / 4)) * sizeof(float2);
@@ -313,6 +314,7 @@ int launch_whiten_any(dp_ctx *c, const Args &a, cudaStream_t st);
 int launch_gram_tc2_any(dp_ctx *c, const Args &b, cudaStream_t st);   // b.S % 32 == 0, U in {16, 32}
 bool precode_tc2_ok(const dp_ctx *c, const Args &a);
 int lsa_setup(dp_ctx *c);
+int fd_rep(const dp_ctx *c, const Args &a, int nw);
 void lsa_teardown(dp_ctx *c);
 int launch_solve_lsa(dp_ctx *c, const Args &a, int sc0, cudaStream_t st);
 int launch_precode_tc2(dp_ctx *c, const Args &a, cudaStream_t st);

@@ -5,17 +5,35 @@
 
 namespace dpi {
 
+// Sub-groups per problem of fd_fused_kernel: replicate while the grid would have fewer than two
+// waves of warps (12 resident per SM), every lane keeps at least two precode rows (the replicas
+// repeat the sweep and the whitening, which must stay the smaller part: cfg2 FD with 16 rows was
+// 18.9 -> 23.7 us at R = 2, fig2a FD with 128 rows 53.7 -> 44.2 us, cfg2 PD single pass with 64 rows
+// 19.0 -> 16.9 us at R = 4), and the replicas fit in one warp (DP_FD_REP=<R> forces R for A/B runs).
+int fd_rep(const dp_ctx *c, const Args &a, int nw) {
+  const int U = c->cfg.U, PPW = 32 / U;
+  static const int env = getenv("DP_FD_REP") ? atoi(getenv("DP_FD_REP")) : 0;
+  const long long nprob = (long long)a.n_sc * a.nchunks, target = 2LL * 12 * c->num_sms;
+  auto fits = [&](int R) { return R <= PPW && (nw * PPW) % R == 0 && a.S % R == 0 && a.S >= 2 * R * U; };
+  if (env > 0) return fits(env) ? env : 1;
+  int R = 1;
+  while (fits(2 * R) && nprob * 2 * R * U / 32 <= target) R *= 2;
+  return R;
+}
+
 template <int U, int KC>
 int launch_fd_fused(dp_ctx *c, const Args &a, cudaStream_t st, int nw_, int kid) {
   const int nw = nw_ > 0 ? nw_ : c->fd_nw;
-  const int nsg = nw * (32 / U);
+  Args b = a;
+  b.rep = fd_rep(c, a, nw);
+  const int npb = nw * (32 / U) / b.rep;                  // problems per CTA
   const int nprob = a.n_sc * a.nchunks;
   static const size_t pad = getenv("DP_FD_SMEM_PAD") ? (size_t)atoi(getenv("DP_FD_SMEM_PAD")) : 0;   // occupancy experiments
-  const size_t sm = smem_fd_fused(U, a.S, a.K, nw) + pad;
+  const size_t sm = smem_fd_fused(U, a.S, a.K, nw, b.rep) + pad;
   auto kern = dpk::fd_fused_kernel<U, KC>;
   CK(set_smem(kern, sm));
   LaunchScope ls(c, kid, st);
-  CK(launch_pdl(kern, dim3((nprob + nsg - 1) / nsg), dim3(nw * 32), sm, st, a));
+  CK(launch_pdl(kern, dim3((nprob + npb - 1) / npb), dim3(nw * 32), sm, st, b));
   return DP_OK;
 }
 template <int U, int KC> struct FdFused {

@@ -682,11 +682,12 @@ __device__ __forceinline__ void transpose_s(const float2 *ss, float2 *sT, int K,
 // Writes x[k * xstride + r]; returns the lane's sum of |x|^2.
 template <int U, int KC>
 __device__ __forceinline__ float precode_sg(const float2 *tile, int row0, int nrows, const float2 *zT, int K,
-                                            float2 *__restrict__ x, size_t xstride, int l, int zs_ = 0) {
+                                            float2 *__restrict__ x, size_t xstride, int l, int zs_ = 0,
+                                            int rfirst = -1, int rstep = U) {
   constexpr int KCP = ZL<KC>::KCP;
   const int zs = zs_ ? zs_ : ZL<KC>::zs(K);
   float pw = 0.f;
-  for (int r = l; r < nrows; r += U) {
+  for (int r = rfirst < 0 ? l : rfirst; r < nrows; r += rstep) {
     const int b = row0 + r;
     const float2 *row = tile + (size_t)b * U;
     const int sw = swz<U>(b);
@@ -753,6 +754,7 @@ struct Args {
   int pf_dist;          // fd_tc: L2-prefetch the tiles of CTA blockIdx.x + pf_dist (0: off)
   int fold;             // fd_tc: per-subcarrier scalars in-kernel (CTAs per subcarrier; 0 = finish kernel)
   int hrow_off;         // host only: H rows before a.H in its allocation (unequal-cluster runs; TMA extent)
+  int rep;              // fd_fused: sub-groups per problem (1, 2, 4, 8; 0 = 1), see fd_fused_kernel
   double kappa64, coef64;   // DP_FLAG_FP64 kernels (f64.cuh): kappa and coef unrounded
 };
 
@@ -792,34 +794,42 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   extern __shared__ __align__(16) float2 smem[];
   const int nw = blockDim.x >> 5;
   const int NSG = nw * PPW;
+  // R = a.rep sub-groups (replicas) per problem, consecutive lane groups of one warp: the antenna
+  // rows of the Gram and of the precode are split over them (their Gram partials summed by a
+  // butterfly, identical in every replica), the U x U sweep and the whitening run in every replica
+  // (same operands, same results); replica 0 writes the scalars.  R > 1 gives the small problems
+  // (U <= 16, few rows per lane) R times the lanes: shorter dependent chains and more warps.
+  const int R = a.rep > 1 ? a.rep : 1;
+  const int NPB = NSG / R;                                // problems per CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sg = warp * PPW + lane / U, l = lane % U;
+  const int q = sg / R, rj = sg % R;                      // problem within the CTA, replica
   const int nprob = a.n_sc * a.nchunks;
-  const int p0 = blockIdx.x * NSG;
-  const int np = min(NSG, nprob - p0);
+  const int p0 = blockIdx.x * NPB;
+  const int np = min(NPB, nprob - p0);
   const int scr_sz = fd_scr_size<U, KC>(a.K);
   const int tile_sz = a.S * U;
-  float2 *tile = smem + (size_t)sg * (tile_sz + scr_sz);
-  float2 *scr = tile + tile_sz;
+  const int pstride = tile_sz + R * scr_sz;               // per problem: [tile][R scratch]
+  float2 *tile = smem + (size_t)q * pstride;
+  float2 *scr = tile + tile_sz + (size_t)rj * scr_sz;
   {
     if (a.Bl == a.nchunks * a.S) {   // clusters contiguous in H: problem p at p S rows
       const float2 *g = a.H + (size_t)p0 * tile_sz;
-      for (int q = 0; q < np; ++q)
-        load_tile_async<U>(smem + (size_t)q * (tile_sz + scr_sz), g + (size_t)q * tile_sz, a.S, threadIdx.x,
-                           blockDim.x);
+      for (int qq = 0; qq < np; ++qq)
+        load_tile_async<U>(smem + (size_t)qq * pstride, g + (size_t)qq * tile_sz, a.S, threadIdx.x, blockDim.x);
     } else {                         // a run of unequal clusters: cluster (sc, cl) at rows sc Bl + cl S
-      for (int q = 0; q < np; ++q) {
-        const int pq = p0 + q;
+      for (int qq = 0; qq < np; ++qq) {
+        const int pq = p0 + qq;
         const float2 *g = a.H + ((size_t)(pq / a.nchunks) * a.Bl + (size_t)(pq % a.nchunks) * a.S) * U;
-        load_tile_async<U>(smem + (size_t)q * (tile_sz + scr_sz), g, a.S, threadIdx.x, blockDim.x);
+        load_tile_async<U>(smem + (size_t)qq * pstride, g, a.S, threadIdx.x, blockDim.x);
       }
     }
     cp_async_wait_all();
     __syncthreads();
   }
-  // Inactive SGs (tail CTA) run the warp-synchronous code on SG 0's data and write nothing.
-  const bool active = sg < np;
-  const int p = active ? p0 + sg : p0;
+  // Inactive SGs (tail CTA) run the warp-synchronous code on problem 0's data and write nothing.
+  const bool active = q < np;
+  const int p = active ? p0 + q : p0;
   if (!active) tile = smem;
   const int sc = p / a.nchunks, cl = p % a.nchunks;
   float2 *slot = scr, *T = scr + 2 * U, *ss = scr + 2 * U, *zT = ss + a.K * U;
@@ -827,7 +837,20 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   {
     GAcc<U> g;
     g.zero();
-    gram_sg<U>(tile, 0, a.S, l, g);
+    const int rows = a.S / R;                             // host: S % R == 0
+    gram_sg<U>(tile, rj * rows, rows, l, g);
+    for (int m = U; m < R * U; m <<= 1) {                 // sum the replicas' partials (butterfly)
+#pragma unroll
+      for (int i = 0; i < U / 2; ++i) {
+        g.top[i].x += __shfl_xor_sync(0xffffffffu, g.top[i].x, m);
+        g.top[i].y += __shfl_xor_sync(0xffffffffu, g.top[i].y, m);
+      }
+#pragma unroll
+      for (int i = 0; i < U / 4; ++i) {
+        g.br[i].x += __shfl_xor_sync(0xffffffffu, g.br[i].x, m);
+        g.br[i].y += __shfl_xor_sync(0xffffffffu, g.br[i].y, m);
+      }
+    }
     gacc_to_column<U>(g, T, l, a.kappa, col);
   }
   // stage s_k of this subcarrier into the (now free) T region while the sweep runs
@@ -856,20 +879,21 @@ __global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
   float pw = 0.f;
   if (active)
     pw = precode_sg<U, KC>(tile, 0, a.S, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
-                           (size_t)a.Bl, l, zs);
+                           (size_t)a.Bl, l, zs, rj * U + l, R * U);
   pw = sg_sum<U>(pw);
-  if (active && l == 0) {
+  for (int m = U; m < R * U; m <<= 1) pw += __shfl_xor_sync(0xffffffffu, pw, m);
+  if (active && l == 0 && rj == 0) {
     a.beta[p] = ok ? beta : qnan();
     a.pw[p] = pw;
     if (!ok) atomicAdd(a.bad, 1);
   }
   if (a.fold) {
-    // the CTA's NSG problems are whole subcarriers (NSG % nchunks == 0): per-subcarrier scalars
+    // the CTA's NPB problems are whole subcarriers (NPB % nchunks == 0): per-subcarrier scalars
     // here, in the order of finish_sc (ascending cluster), instead of fd_finish_kernel
     __shared__ float fb[32], fp[32];
-    if (l == 0) { fb[sg] = 1.f / (ok ? beta : qnan()); fp[sg] = pw; }
+    if (l == 0 && rj == 0) { fb[q] = 1.f / (ok ? beta : qnan()); fp[q] = pw; }
     __syncthreads();
-    const int per = NSG / a.nchunks;
+    const int per = NPB / a.nchunks;
     if ((int)threadIdx.x < per) {
       const int q0 = threadIdx.x * a.nchunks;
       if (p0 + q0 < nprob) {
