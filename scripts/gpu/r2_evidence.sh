@@ -1,0 +1,8 @@
+# round-2 evidence: GPU tests, default bench line, reference arm, launch list, ncu of the cfg4 kernels
+TAG=${TAG:-r02f}
+timeout 500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc $?" >> gpurun_out/${TAG}_pytest.log
+timeout 400 python bench.py > gpurun_out/${TAG}_b4.json 2> gpurun_out/${TAG}_b4.err
+timeout 300 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 2 --profile-run > /dev/null 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k 'regex:fd_tc|gram_tc2|solve_mw|precode_tc2' -s 8 -c 4 -o gpurun_out/${TAG}_cfg4 python bench.py --steps 2 --warmup 2 --profile-run > /dev/null 2>&1
+ls -la gpurun_out | grep $TAG

@@ -56,6 +56,7 @@ CASES = [
     (CONFIGS[4], 29),        # U=32, S=32 = U
     (PAPER_POINTS["fig2a"], 23),   # U=16, S=128, K=7
     (PAPER_POINTS["fig2e"], 19),   # U=16, S=32, K=7
+    (PAPER_POINTS["fig2d"], 27),   # U=16, B=64: PD single pass at world 1, rows over 2 sub-groups
 ]
 
 
