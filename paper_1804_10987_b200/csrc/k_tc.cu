@@ -73,10 +73,12 @@ bool precode_tc2_ok(const dp_ctx *c, const Args &a) {
 int launch_precode_tc2(dp_ctx *c, const Args &a, cudaStream_t st) {
   CUtensorMap tm;
   RET(make_h_tmap(c, a.H, a.n_sc * a.Bl, &tm, dpk::PC2_ROWS, CU_TENSOR_MAP_SWIZZLE_128B));
-  auto kern = dpk::precode_tc2_kernel;
-  CK(set_smem(kern, dpk::PC2_SMEM));
+  static const bool smem_hs = getenv("DP_PC2_SMEM_HS") != nullptr;   // A/B: residual plane in shared memory
+  auto kern = smem_hs ? dpk::precode_tc2_kernel<false> : dpk::precode_tc2_kernel<true>;
+  const size_t smem = dpk::pc2_smem(!smem_hs);
+  CK(set_smem(kern, smem));
   LaunchScope ls(c, DP_KERNEL_PRECODE, st);
-  CK(launch_pdl(kern, dim3(std::min(a.n_sc, c->num_sms)), dim3(dpk::PC2_THREADS), dpk::PC2_SMEM, st, tm, a));
+  CK(launch_pdl(kern, dim3(std::min(a.n_sc, c->num_sms)), dim3(dpk::PC2_THREADS), smem, st, tm, a));
   return DP_OK;
 }
 

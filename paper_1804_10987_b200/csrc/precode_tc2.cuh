@@ -27,6 +27,14 @@
 //   warp 9     UMMA issuer: 16 UMMAs per block into a double-buffered TMEM accumulator.
 //   warps 0-3  epilogue: TMEM lane quarter -> x rows (coalesced: one antenna per lane),
 //              the subcarrier's power, and its per-subcarrier scalars (fin).
+//
+// HT = true (the default): the residual plane Hs goes to TMEM instead of a shared-memory buffer.
+// The prep warp of lane quarter q reads antenna row 32q + lane of the raw block (16 16-byte loads
+// of its own row), forms Hs in registers and stores its 64 reals as 64 TMEM columns of its lane;
+// the Hs Zb^T product is then a .ts UMMA with A from TMEM (M = 128 antenna rows, K = 64 reals).
+// That removes the shared-memory write of Hs and the UMMA's shared-memory read of it (the
+// ablation of DESIGN.md §7 charges 3.8 us of 29.2 to the residual round trip) and frees the two
+// 32 KB Hs buffers for two more raw ring stages (6 x 32 KB of H in flight).
 #pragma once
 
 // diagnostics only (scripts/gram_diag.sh builds, never the shipped build): 1 = no UMMAs, 2 = no UMMAs
@@ -45,28 +53,41 @@ constexpr int PC2_BOX = PC2_ROWS * 128;         // one TMA box: 128 rows x 32 fp
 constexpr int PC2_STAGE = 2 * PC2_BOX;          // Hb: 2 K-halves = 32 KB (Hs buffers: same size)
 constexpr int PC2_ZOP = 64 * 64 * 4;            // Z' operand: 64 rows (Zb 0..31, Zs 32..63) x 64 K (x2 buffers)
 constexpr int PC2_THREADS = 320;
-constexpr size_t PC2_SMEM = (size_t)(PC2_NS + PC2_NH) * PC2_STAGE + 2 * PC2_ZOP + 1024;
+__host__ __device__ constexpr int pc2_ns(bool ht) { return ht ? PC2_NS + PC2_NH : PC2_NS; }   // raw stages
+__host__ __device__ constexpr size_t pc2_smem(bool ht) {
+  return (size_t)(PC2_NS + PC2_NH) * PC2_STAGE + 2 * PC2_ZOP + 1024;   // HT: the Hs buffers become raw stages
+}
+constexpr size_t PC2_SMEM = pc2_smem(false);
 
+// byte offset of 16-byte chunk c (reals 4c..4c+3, c < 16) of row r in a K-major SWIZZLE_128B block
+// of PC2_ROWS rows (two 16 KB boxes of 32 reals)
+__device__ __forceinline__ uint32_t pc2_chunk(int r, int c) {
+  return (uint32_t)((c >> 3) * PC2_BOX + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+template <bool HT>
 __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __grid_constant__ CUtensorMap tmH, Args a) {
   pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
                    // (it still waits for this grid's completion in griddepcontrol.wait)
+  constexpr int NS = pc2_ns(HT);
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t *sm = smem_dyn + ((1024u - (tc::smem_u32(smem_dyn) & 1023u)) & 1023u);
-  uint8_t *hsb = sm + (size_t)PC2_NS * PC2_STAGE;   // residual buffers
-  uint8_t *zop = hsb + (size_t)PC2_NH * PC2_STAGE;   // Z' double buffer
-  __shared__ __align__(8) uint64_t full[PC2_NS], stage_free[PC2_NS], hs_full[PC2_NH], hs_free[PC2_NH];
+  uint8_t *hsb = sm + (size_t)PC2_NS * PC2_STAGE;   // residual buffers (!HT)
+  uint8_t *zop = sm + (size_t)(PC2_NS + PC2_NH) * PC2_STAGE;   // Z' double buffer
+  __shared__ __align__(8) uint64_t full[NS], stage_free[NS], hs_full[PC2_NH], hs_free[PC2_NH];
   __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2], zready[2], zfree[2];
   __shared__ uint32_t tmem_base;
   __shared__ float pw_red[4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nblk = a.Bl / PC2_ROWS;
   const int n_items = a.n_sc;
+  constexpr uint32_t TCOLS = HT ? 256 : 128;        // D double buffer (+ HT: Hs double buffer at 128 + 64 b)
   if (warp == 0) {
-    tc::tmem_alloc(&tmem_base, 128);
+    tc::tmem_alloc(&tmem_base, TCOLS);
     tc::tmem_relinquish();
   }
   if (tid == 32) {
-    for (int i = 0; i < PC2_NS; ++i) {
+    for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&full[i], 1);
       tc::mbar_init(&stage_free[i], 1);
     }
@@ -93,13 +114,13 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
       int s = 0, ph = 0, g = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         for (int blk = 0; blk < nblk; ++blk, ++g) {
-          if (g >= PC2_NS) tc::mbar_wait(&stage_free[s], ph ^ 1);
+          if (g >= NS) tc::mbar_wait(&stage_free[s], ph ^ 1);
           uint8_t *st = sm + (size_t)s * PC2_STAGE;
           const int row0 = item * a.Bl + blk * PC2_ROWS;
           tc::mbar_arrive_expect_tx(&full[s], 2 * PC2_BOX);
           tc::tma_load_2d(st, &tmH, 0, row0, &full[s]);
           tc::tma_load_2d(st + PC2_BOX, &tmH, 32, row0, &full[s]);
-          if (++s == PC2_NS) { s = 0; ph ^= 1; }
+          if (++s == NS) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -127,13 +148,14 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
             const uint64_t zd = tc::smem_desc(zo + t * 2 * 64 * 16, 64 * 16, 128);
             if (DP_PC2_DIAG < 1) {
               tc::mma_tf32(d, tc::smem_desc_sw128(hb + koff, 1024), zd, ID64, t > 0 ? 1u : 0u);
-              tc::mma_tf32(d, tc::smem_desc_sw128(hs + koff, 1024), zd, ID32, 1u);
+              if (HT) tc::mma_tf32_ts(d, tm + 128 + 64 * b + 8 * t, zd, ID32, 1u);   // Hs from TMEM
+              else tc::mma_tf32(d, tc::smem_desc_sw128(hs + koff, 1024), zd, ID32, 1u);
             }
           }
           tc::mma_commit(&stage_free[s]);
           tc::mma_commit(&hs_free[b]);
           tc::mma_commit(&acc_full[b]);
-          if (++s == PC2_NS) { s = 0; ph ^= 1; }
+          if (++s == NS) { s = 0; ph ^= 1; }
         }
         tc::mma_commit(&zfree[n & 1]);
       }
@@ -178,24 +200,43 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
         tc::mbar_wait(&full[s], ph);
         if (g >= PC2_NH) tc::mbar_wait(&hs_free[hbuf], ((g >> 1) - 1) & 1);
         uint8_t *st = sm + (size_t)s * PC2_STAGE;
-        const uint4 *src = reinterpret_cast<const uint4 *>(st);
-        uint4 *dst = reinterpret_cast<uint4 *>(hsb + (size_t)hbuf * PC2_STAGE);
-        constexpr int NV = DP_PC2_DIAG >= 2 ? 0 : 2 * PC2_BOX / 16 / 128;      // 16 vectors per thread
-        uint4 v[NV > 0 ? NV : 1];
+        if constexpr (HT) {
+          // this lane's antenna row r of the block: Hs = H - trunc_tf32(H) -> TMEM lane r, columns = reals
+          const int r = ptid;                                  // warp 4 + q holds rows 32 q .. (its lane quarter)
+          float h[64];
 #pragma unroll
-        for (int i = 0; i < NV; ++i) v[i] = src[ptid + 128 * i];
+          for (int c = 0; c < 16; ++c) {
+            const float4 v = *reinterpret_cast<const float4 *>(st + pc2_chunk(r, c));
+            h[4 * c] = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+            h[4 * c + 1] = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+            h[4 * c + 2] = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+            h[4 * c + 3] = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          }
+          const uint32_t th = tm + 128 + 64 * hbuf + ((uint32_t)(32 * (warp - 4)) << 16);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {                  // Hs = H - trunc_tf32(H), same swizzled positions
-          float4 f;
-          f.x = __uint_as_float(v[i].x) - __uint_as_float(v[i].x & 0xFFFFE000u);
-          f.y = __uint_as_float(v[i].y) - __uint_as_float(v[i].y & 0xFFFFE000u);
-          f.z = __uint_as_float(v[i].z) - __uint_as_float(v[i].z & 0xFFFFE000u);
-          f.w = __uint_as_float(v[i].w) - __uint_as_float(v[i].w & 0xFFFFE000u);
-          dst[ptid + 128 * i] = *reinterpret_cast<uint4 *>(&f);
+          for (int cb = 0; cb < 4; ++cb) tc::tmem_st16(th + 16 * cb, *reinterpret_cast<float(*)[16]>(h + 16 * cb));
+          tc::tmem_wait_st();
+          tc::fence_before_sync();
+        } else {
+          const uint4 *src = reinterpret_cast<const uint4 *>(st);
+          uint4 *dst = reinterpret_cast<uint4 *>(hsb + (size_t)hbuf * PC2_STAGE);
+          constexpr int NV = DP_PC2_DIAG >= 2 ? 0 : 2 * PC2_BOX / 16 / 128;      // 16 vectors per thread
+          uint4 v[NV > 0 ? NV : 1];
+#pragma unroll
+          for (int i = 0; i < NV; ++i) v[i] = src[ptid + 128 * i];
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {                  // Hs = H - trunc_tf32(H), same swizzled positions
+            float4 f;
+            f.x = __uint_as_float(v[i].x) - __uint_as_float(v[i].x & 0xFFFFE000u);
+            f.y = __uint_as_float(v[i].y) - __uint_as_float(v[i].y & 0xFFFFE000u);
+            f.z = __uint_as_float(v[i].z) - __uint_as_float(v[i].z & 0xFFFFE000u);
+            f.w = __uint_as_float(v[i].w) - __uint_as_float(v[i].w & 0xFFFFE000u);
+            dst[ptid + 128 * i] = *reinterpret_cast<uint4 *>(&f);
+          }
+          tc::fence_proxy_async();
         }
-        tc::fence_proxy_async();
         mbar_arrive(&hs_full[hbuf]);
-        if (++s == PC2_NS) { s = 0; ph ^= 1; }
+        if (++s == NS) { s = 0; ph ^= 1; }
       }
     }
   } else {
@@ -240,7 +281,7 @@ __global__ void __launch_bounds__(PC2_THREADS, 1) precode_tc2_kernel(const __gri
   pdl_trigger();
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tm, 128);
+  if (warp == 0) tc::tmem_dealloc(tm, TCOLS);
 }
 
 }  // namespace dpk
