@@ -35,11 +35,26 @@
 
 namespace dpk {
 
+// many-waiter completions (every warp of the CTA waits): parked try_wait (DP_FD_SPIN: plain polling)
+#ifndef DP_FD_ABL
+#define DP_FD_ABL 0   // diagnostics builds only: 1 no sweep, 2 no SIMT precode, 4 no Gram UMMAs (timing ablation)
+#endif
+#ifdef DP_FD_SPIN
+#define WAITF tc::mbar_wait
+#else
+#define WAITF tc::mbar_wait_park
+#endif
+
 constexpr int FDT_TILE = 8192;                 // 32 rows x 64 fp32, two SW128 boxes of 4 KB
 constexpr int FDT_REG = 9216;                  // per-warp region (1024-aligned)
 constexpr int FDT_GLD = 34;                    // G staging column stride (complex), 272 B
 constexpr int FDT_THREADS = 128;
-constexpr size_t FDT_SMEM = 4 * FDT_TILE + 4 * FDT_REG + 4 * 64 * 8 + 1024;
+#ifdef DP_FD_SWEEP2D
+constexpr int FDT_SLOT = 1280;                // per problem: 4 pivot-row buffers of 36 complex + 32 row scales (sweep_2d)
+#else
+constexpr int FDT_SLOT = 512;                 // per problem: 2 pivot-row buffers of 32 complex (sweep_sg2)
+#endif
+constexpr size_t FDT_SMEM = 4 * FDT_TILE + 4 * FDT_REG + 4 * FDT_SLOT + 1024;
 
 // UMMA shared-memory descriptor of an MN-major SWIZZLE_128B_BASE32B operand: 128-byte
 // rows along MN (32 tf32), 4-row K groups SBO bytes apart, MN atoms LBO bytes apart.
@@ -112,6 +127,142 @@ __device__ __forceinline__ float precode_sw128(const uint8_t *tile, const float2
   return pw;
 }
 
+// 2-D register-blocked Hermitian sweep for U = 32, one warp per problem (the Gauss-Jordan sweep of
+// sweep_sg2 on the Jacobi-equilibrated A, P:285-286 / Lemma 1).  Lane (r, c) = (lane >> 3, lane & 7)
+// owns the 8 x 4 block rows 8r .. 8r+7, columns 4c .. 4c+3 of A.  Per pivot k a lane needs only the
+// pivot-row entries of its 8 rows (the pivot column, by Hermitian symmetry) and of its 4 columns:
+// 6 16-byte loads (12 shared-memory wavefronts) instead of the 16 broadcast loads (32 wavefronts)
+// of the column-per-lane sweep, for the same 64 FFMA2.
+//   Update (i, j != k):  a_ij -= conj(R_i) sig_j,  sig_j = R_j / d  (sig_k = 1 - 1/d: column k
+//   becomes a_ik / d),  R = pivot row k, d = a_kk.  Row k (a_kj -> a_kj / d) takes the same update
+//   with R_k replaced by d - 1 (a_kj - (d - 1) a_kj / d = a_kj / d); the pivot entry is set to -1/d.
+// The next pivot row is updated first (look-ahead) and published by its 8 owner lanes into one of
+// four rotating row buffers (one __syncwarp per pivot).  Row-buffer position of entry j: j + 2 (j >> 4)
+// (a 16-byte gap after 16 entries keeps the column-part loads of the 8 column groups conflict-free).
+// In: g = G staging of the problem (column j at g + j * FDT_GLD, complex), A = G + kappa I.
+// Out: g columns = -A^{-1} (zeroed when not HPD); returns beta (Lemma 1, Eq. 6).
+__device__ __forceinline__ int rbpos(int j) { return j + 2 * (j >> 4); }
+__device__ __forceinline__ float sweep_2d(float2 *g, uint8_t *sl, int lane, float kappa, float coef, bool &ok) {
+  const int r = lane >> 3, c = lane & 7;
+  float2 *buf = reinterpret_cast<float2 *>(sl);               // [4][36]
+  float *rs = reinterpret_cast<float *>(sl + 4 * 36 * 8);     // [32] row / column scales
+  const float dl = g[lane * FDT_GLD + lane].x + kappa;        // own diagonal (lane = column index)
+  const bool gd = (dl > 0.f) && (dl < INFINITY);
+  rs[lane] = gd ? rsqrtf(dl) : 1.f;
+  float2 w[8][4];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const float2 *col = g + (4 * c + jj) * FDT_GLD + 8 * r;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const float4 v = *reinterpret_cast<const float4 *>(col + 2 * m);
+      w[2 * m][jj] = lo2(v);
+      w[2 * m + 1][jj] = hi2(v);
+    }
+  }
+  const bool hasdiag = (c >> 1) == r;                          // block holds (4c + jj, 4c + jj)
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    if (hasdiag && !(c & 1)) w[jj][jj] = make_float2(w[jj][jj].x + kappa, 0.f);
+    if (hasdiag && (c & 1)) w[4 + jj][jj] = make_float2(w[4 + jj][jj].x + kappa, 0.f);
+  }
+  __syncwarp();
+  float rr[8], rc[4];
+  {
+    const float4 a0 = *reinterpret_cast<const float4 *>(rs + 8 * r), a1 = *reinterpret_cast<const float4 *>(rs + 8 * r + 4);
+    const float4 b0 = *reinterpret_cast<const float4 *>(rs + 4 * c);
+    rr[0] = a0.x; rr[1] = a0.y; rr[2] = a0.z; rr[3] = a0.w; rr[4] = a1.x; rr[5] = a1.y; rr[6] = a1.z; rr[7] = a1.w;
+    rc[0] = b0.x; rc[1] = b0.y; rc[2] = b0.z; rc[3] = b0.w;
+  }
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) w[ii][jj] = cscale(w[ii][jj], rr[ii] * rc[jj]);
+  const int cpos = 4 * c + 2 * (c >> 2), rpos = 8 * r + 2 * (r >> 1);
+  if (r == 0) {                                               // row 0 opens the sweep
+    *reinterpret_cast<float4 *>(buf + cpos) = make_float4(w[0][0].x, w[0][0].y, w[0][1].x, w[0][1].y);
+    *reinterpret_cast<float4 *>(buf + cpos + 2) = make_float4(w[0][2].x, w[0][2].y, w[0][3].x, w[0][3].y);
+  }
+  __syncwarp();
+  float pmin = buf[0].x, pmax = pmin;
+  float id = rcp_approx(pmin);
+#pragma unroll 1
+  for (int kk = 0; kk < 32; kk += 8) {
+    const bool pr = (r == (kk >> 3));                          // this block's pivot rows are my rows
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = kk + j;
+      const float2 *cur = buf + 36 * (j & 3);
+      float2 *nxt = buf + 36 * ((j + 1) & 3);
+      const float4 c01 = *reinterpret_cast<const float4 *>(cur + cpos);
+      const float4 c23 = *reinterpret_cast<const float4 *>(cur + cpos + 2);
+      float2 R[8];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const float4 v = *reinterpret_cast<const float4 *>(cur + rpos + 2 * m);
+        R[2 * m] = lo2(v);
+        R[2 * m + 1] = hi2(v);
+      }
+      float2 sg[4] = {cscale(lo2(c01), id), cscale(hi2(c01), id), cscale(lo2(c23), id), cscale(hi2(c23), id)};
+      const bool pc = (c == (k >> 2));                         // my columns hold column k (jj = k & 3)
+      if (pc) sg[j & 3] = make_float2(1.f - id, 0.f);
+      if (pr) R[j].x -= 1.f;                                   // row k: d -> d - 1
+      const int jn = (j + 1) & 7;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) cfms_cj(w[jn][jj], R[jn], sg[jj]);   // row k+1 first
+      const bool pn = (j < 7) ? pr : (r == (kk >> 3) + 1);     // my rows hold row k+1
+      if (pn && k + 1 < 32) {
+        *reinterpret_cast<float4 *>(nxt + cpos) = make_float4(w[jn][0].x, w[jn][0].y, w[jn][1].x, w[jn][1].y);
+        *reinterpret_cast<float4 *>(nxt + cpos + 2) = make_float4(w[jn][2].x, w[jn][2].y, w[jn][3].x, w[jn][3].y);
+      }
+      __syncwarp();
+      float idn = 1.f;
+      if (k + 1 < 32) {
+        const float dn = nxt[rbpos(k + 1)].x;                 // a_{k+1,k+1}
+        pmin = fminf(pmin, dn);
+        pmax = fmaxf(pmax, dn);
+        idn = rcp_approx(dn);
+      }
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii)
+        if (ii != jn)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) cfms_cj(w[ii][jj], R[ii], sg[jj]);
+      if (pr && pc) w[j][j & 3] = make_float2(-id, 0.f);      // the pivot entry
+      id = idn;
+    }
+  }
+  // undo the equilibration: A^{-1} = D^{-1/2} A'^{-1} D^{-1/2}; Lemma 1 traces
+  float tr = 0.f, f = 0.f;
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      w[ii][jj] = cscale(w[ii][jj], rr[ii] * rc[jj]);
+      f += cabs2(w[ii][jj]);
+    }
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    if (hasdiag && !(c & 1)) tr -= w[jj][jj].x;
+    if (hasdiag && (c & 1)) tr -= w[4 + jj][jj].x;
+  }
+  tr = sg_sum<32>(tr);
+  f = sg_sum<32>(f);
+  // Lemma 1, Eq. (6):  beta^2 = Es/rho^2 (tr A^{-1} - kappa ||A^{-1}||_F^2)
+  const float rad = coef * (tr - kappa * f);
+  const bool all_gd = __all_sync(0xffffffffu, gd);
+  ok = all_gd && (pmin > 0.f) && (pmax < INFINITY) && (rad > 0.f) && (rad < INFINITY);
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    float2 *col = g + (4 * c + jj) * FDT_GLD + 8 * r;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      *reinterpret_cast<float4 *>(col + 2 * m) =
+          ok ? make_float4(w[2 * m][jj].x, w[2 * m][jj].y, w[2 * m + 1][jj].x, w[2 * m + 1][jj].y) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  return ok ? sqrtf(rad) : 1.f;
+}
+
 // Per-subcarrier scalars folded into the FD kernel (replaces fd_finish_kernel):
 // fin[sc] = {sum_c 1/beta_c, sum_c power_c} over the rank's Cl clusters, ascending c
 // (the order of finish_sc, so the result is bit-identical).  a.fold = CTAs per
@@ -153,8 +304,9 @@ __device__ __forceinline__ void fd_fold_init(const Args &a, FoldSmem &f) {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // init already fenced (fence.mbarrier_init)
   }
 }
-__device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p0, int warp, int lane, float ib, float pw) {
-  if (lane == 0) { f.fb[warp] = ib; f.fp[warp] = pw; }
+__device__ __forceinline__ void fd_fold_finish(const Args &a, FoldSmem &f, int p0, int warp, int lane, float ib, float pw,
+                                               bool writer = true) {
+  if (lane == 0 && writer) { f.fb[warp] = ib; f.fp[warp] = pw; }   // warp = the problem's slot 0..3
   __syncthreads();
   const int nprob = a.n_sc * a.nchunks;
   if (a.fold == 1) {
@@ -246,7 +398,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   const uint8_t *tl = tile(p);
   uint8_t *rg = region(p);
   if (active) {
-    tc::mbar_wait(&tile_full[p], 0);
+    WAITF(&tile_full[p], 0);
     const uint4 *src = reinterpret_cast<const uint4 *>(tl);
     float4 *dst = reinterpret_cast<float4 *>(rg);
     uint4 v16[FDT_TILE / 16 / 32];
@@ -275,6 +427,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
       for (int t = 0; t < 4; ++t) {                            // antennas 8t .. 8t+7
         const uint64_t b = smem_desc_mn_sw128b32(xb + 1024 * t, 4096, 512);
         const uint64_t s = smem_desc_mn_sw128b32(xs + 1024 * t, 4096, 512);
+        if (DP_FD_ABL & 4) continue;
         tc::mma_tf32(d, b, b, IDESC, t > 0 ? 1u : 0u);         // Xb^T Xb
         tc::mma_tf32(d, s, b, IDESC, 1u);                      // Xs^T Xb
         tc::mma_tf32(d, b, s, IDESC, 1u);                      // Xb^T Xs
@@ -283,7 +436,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     tc::mma_commit(&mma_done);
   }
   __syncwarp();
-  tc::mbar_wait(&mma_done, 0);
+  WAITF(&mma_done, 0);
   tc::fence_after_sync();
   // ---- epilogue: TMEM lane 32 warp + i holds P row r = 16 warp + (i & 15) of problem
   // 2 g + (i >> 4) in columns 64 g .. 64 g + 63 (two M = 64 accumulators share columns)
@@ -342,27 +495,46 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   // ---------------------------------------------------------------- SIMT solver
   const int sc = (active ? pr : p0) / a.nchunks, cl = pr % a.nchunks;
   const int l = lane;
-  float2 *slot = reinterpret_cast<float2 *>(sm + 4 * FDT_TILE + 4 * FDT_REG) + 64 * p;
+  uint8_t *slot8 = sm + 4 * FDT_TILE + 4 * FDT_REG + (size_t)p * FDT_SLOT;
+  float2 *slot = reinterpret_cast<float2 *>(slot8);
   float2 col[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) col[u] = make_float2(0.f, 0.f);
-  float dl = 1.f;
-  if (active) {
-    float2 *g = reinterpret_cast<float2 *>(rg) + l * FDT_GLD;
-    dl = g[l].x + a.kappa;
-    g[l] = make_float2(dl, 0.f);                                // A = G_c + kappa_c I (own row only)
-#pragma unroll
-    for (int u = 0; u < U; u += 2) {
-      const float4 v = *reinterpret_cast<const float4 *>(g + u);
-      col[u] = lo2(v);
-      col[u + 1] = hi2(v);
-    }
-  }
-  __syncwarp();
+  bool ok = false;
+  float beta = 1.f;
   // region: [ss (K x U), later zT (U x FDT_SP)] [sT (U x FDT_SP) | WTC: pieces of the s operand]
   float2 *ss = reinterpret_cast<float2 *>(rg), *zT = ss, *sT = ss + U * FDT_SP;
   auto piece = [&](int q) { return region(q >> 2) + 4608 + 1024 * (q & 3); };   // S' piece q = plane * 8 + t
   if constexpr (WTC) {
+    // column-per-lane sweep (sweep_sg2); DP_FD_SWEEP2D (diagnostics builds): the 2-D blocked sweep in
+    // place on the G staging (-A^{-1} columns written back), then column l to lane l for the A' rows
+    float2 *gs = reinterpret_cast<float2 *>(rg);
+    if (DP_FD_ABL & 1) ok = true;
+    else if (active) {
+#ifndef DP_FD_SWEEP2D
+      float2 *g = gs + l * FDT_GLD;
+      const float dl = g[l].x + a.kappa;
+      g[l] = make_float2(dl, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        const float4 v = *reinterpret_cast<const float4 *>(g + u);
+        col[u] = lo2(v);
+        col[u + 1] = hi2(v);
+      }
+      __syncwarp();
+      beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);
+#else
+      beta = sweep_2d(gs, slot8, l, a.kappa, a.coef, ok);
+      __syncwarp();
+      const float2 *g = gs + l * FDT_GLD;
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        const float4 v = *reinterpret_cast<const float4 *>(g + u);
+        col[u] = lo2(v);
+        col[u + 1] = hi2(v);
+      }
+#endif
+    }
     // ---- Whitening on the tensor cores:  Z = A^{-1} S / beta for the CTA's 4 problems at
     // once (they share s: same subcarrier).  Real form with j = 2v + {0: re, 1: im}:
     //   A'[32p + u][j]  = (A_p^{-1}[u][v] / beta_p) (re, im)         M = 128 (4 x 32 rows)
@@ -390,11 +562,23 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     }
     tc::fence_proxy_async();
   } else {
+    float dl = 1.f;
+    if (active) {
+      float2 *g = reinterpret_cast<float2 *>(rg) + l * FDT_GLD;
+      dl = g[l].x + a.kappa;
+      g[l] = make_float2(dl, 0.f);                              // A = G_c + kappa_c I (own row only)
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        const float4 v = *reinterpret_cast<const float4 *>(g + u);
+        col[u] = lo2(v);
+        col[u + 1] = hi2(v);
+      }
+    }
+    __syncwarp();
     sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
+    if (DP_FD_ABL & 1) ok = true;
+    else if (active) beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   }
-  bool ok = false;
-  float beta = 1.f;
-  if (active) beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;       // failed problems: x = 0
   if constexpr (WTC) {
     const uint32_t tq = tm + ((uint32_t)(32 * warp) << 16);  // this warp's TMEM lane quarter
@@ -421,7 +605,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
       }
       tc::mma_commit(&wz_done[0]);
     }
-    tc::mbar_wait(&wz_done[0], 0);
+    WAITF(&wz_done[0], 0);
     tc::fence_after_sync();
 #pragma unroll
     for (int c = 0; c < 4; ++c)
@@ -440,7 +624,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
         tc::mma_tf32_ts(tm + 64, tm + 8 * t, tc::smem_desc(tc::smem_u32(piece(t)), 512, 128), ID, 1u);   // A's S'b
       tc::mma_commit(&wz_done[1]);
     }
-    tc::mbar_wait(&wz_done[1], 0);
+    WAITF(&wz_done[1], 0);
     tc::fence_after_sync();
     float zv[2][16];
     tc::tmem_ld16_nowait(tq + 64, zv[0]);
@@ -474,7 +658,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   }
   __syncwarp();
   if (active) {
-    float pw = precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l, FDT_SP);
+    float pw = (DP_FD_ABL & 2) ? 0.f : precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l, FDT_SP);
     pw = sg_sum<U>(pw);
     if (l == 0) {
       a.beta[pr] = ok ? beta : qnan();

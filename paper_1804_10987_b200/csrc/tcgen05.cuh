@@ -127,6 +127,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
 }
 #endif
 
+// wait with a suspend-time hint: the waiting thread is parked in the try_wait until the phase
+// completes (or ~hint ns pass) instead of re-issuing polls that take issue slots from the
+// co-resident warps (many-waiter barriers: the CTA-wide tensor-core completions of fd_tc2)
+__device__ __forceinline__ void mbar_wait_park(uint64_t *mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITP_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAITP_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
+}
+
 // wait with exponential nanosleep back-off (single-thread producer / issuer roles, so a
 // spinning thread does not steal issue slots from the working warps)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *mbar, uint32_t phase) {
