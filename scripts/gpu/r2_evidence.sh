@@ -1,5 +1,6 @@
 # round-2 evidence: GPU tests, default bench line, reference arm, launch list, ncu of the cfg4 kernels
 TAG=${TAG:-r02f}
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/${TAG}_smoke.log
 timeout 500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc $?" >> gpurun_out/${TAG}_pytest.log
 timeout 400 python bench.py > gpurun_out/${TAG}_b4.json 2> gpurun_out/${TAG}_b4.err
 timeout 300 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
