@@ -127,6 +127,60 @@ __device__ __forceinline__ float precode_sw128(const uint8_t *tile, const float2
   return pw;
 }
 
+// x[k][r] = sum_u conj(H[r][u]) z[k][u] with the symbols split in two halves (WTC path): lane l
+// computes antennas r0 = l & 15 and r1 = r0 + 16 for the symbols kg KH .. kg KH + KH-1 (kg = l >> 4,
+// KH = ceil(KC / 2)), reading z from zT[u][8 kg + m] (the layout fd_tc's tensor-core whitening
+// writes).  Per pair of users: 2 tile loads (rows r0, r1) + 8 z loads for 4 KH complex MACs, against
+// 1 + 2 KH loads for 2 KH MACs with one row per lane (precode_sw128): a third fewer shared-memory
+// loads, the same FFMA2 count.  Rows r0 and r0 + 16 keep the swizzled tile reads at 4 bank positions.
+template <int KC>
+__device__ __forceinline__ float precode_sw128_h(const uint8_t *tile, const float2 *zT, int K, float2 *__restrict__ x,
+                                                 size_t xstride, int l) {
+  constexpr int KH = (KC + 1) / 2;
+  const int r0 = l & 15, r1 = r0 + 16, kg = l >> 4;
+  float2 a0[KH], a1[KH];
+#pragma unroll
+  for (int m = 0; m < KH; ++m) a0[m] = a1[m] = make_float2(0.f, 0.f);
+  const float2 *zq = zT + 8 * kg;
+#pragma unroll 2
+  for (int c = 0; c < 16; ++c) {
+    const float4 h0 = ld_chunk_sw128(tile, r0, c), h1 = ld_chunk_sw128(tile, r1, c);
+    const float2 *za = zq + (2 * c) * FDT_SP, *zb = za + FDT_SP;   // users 2c, 2c+1
+#pragma unroll
+    for (int m = 0; m < KH; m += 2) {
+      if (m + 1 < KH) {
+        const float4 va = *reinterpret_cast<const float4 *>(za + m);
+        const float4 vb = *reinterpret_cast<const float4 *>(zb + m);
+        cfma_cj(a0[m], lo2(h0), lo2(va));
+        cfma_cj(a0[m + 1], lo2(h0), hi2(va));
+        cfma_cj(a1[m], lo2(h1), lo2(va));
+        cfma_cj(a1[m + 1], lo2(h1), hi2(va));
+        cfma_cj(a0[m], hi2(h0), lo2(vb));
+        cfma_cj(a0[m + 1], hi2(h0), hi2(vb));
+        cfma_cj(a1[m], hi2(h1), lo2(vb));
+        cfma_cj(a1[m + 1], hi2(h1), hi2(vb));
+      } else {
+        const float2 va = za[m], vb = zb[m];
+        cfma_cj(a0[m], lo2(h0), va);
+        cfma_cj(a1[m], lo2(h1), va);
+        cfma_cj(a0[m], hi2(h0), vb);
+        cfma_cj(a1[m], hi2(h1), vb);
+      }
+    }
+  }
+  float pw = 0.f;
+#pragma unroll
+  for (int m = 0; m < KH; ++m) {
+    const int k = kg * KH + m;
+    if (k < K) {
+      x[(size_t)k * xstride + r0] = a0[m];
+      x[(size_t)k * xstride + r1] = a1[m];
+      pw += cabs2(a0[m]) + cabs2(a1[m]);
+    }
+  }
+  return pw;
+}
+
 // 2-D register-blocked Hermitian sweep for U = 32, one warp per problem (the Gauss-Jordan sweep of
 // sweep_sg2 on the Jacobi-equilibrated A, P:285-286 / Lemma 1).  Lane (r, c) = (lane >> 3, lane & 7)
 // owns the 8 x 4 block rows 8r .. 8r+7, columns 4c .. 4c+3 of A.  Per pivot k a lane needs only the
@@ -522,6 +576,8 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
         col[u + 1] = hi2(v);
       }
       __syncwarp();
+      // s of this subcarrier -> warp 0's region (free until zT): read by the S' build after the sweep
+      if (warp == 0) sg_copy_async<U>(reinterpret_cast<float2 *>(rg), a.s + (size_t)sc * a.K * U, a.K * U, l);
       beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);
 #else
       beta = sweep_2d(gs, slot8, l, a.kappa, a.coef, ok);
@@ -544,13 +600,23 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     // S' (K-major interleaved, N = 32) in 16 pieces of 1 KB (one per K step and plane)
     // in the regions' second halves.  3xTF32: A'b S'b + A'b S's, then A's S'b after A's
     // replaces A'b in TMEM (TMEM holds 128 columns: A' 64, D 32).
+#ifndef DP_FD_SWEEP2D
+    cp_async_wait_all();                                      // warp 0: the staged s
+#endif
     named_sync(1, 128);                                       // every warp has read its G staging
+#ifndef DP_FD_SWEEP2D
+    const float2 *s_st = reinterpret_cast<const float2 *>(region(0));
+#endif
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int e = tid + 128 * i, n = e >> 5, v = e & 31, k = n & 15;
       float2 w = make_float2(0.f, 0.f);
       if (k < a.K) {
+#ifndef DP_FD_SWEEP2D
+        const float2 sv = s_st[k * U + v];
+#else
         const float2 sv = __ldg(a.s + ((size_t)sc * a.K + k) * U + v);
+#endif
         w = n < 16 ? make_float2(sv.x, -sv.y) : make_float2(sv.y, sv.x);
       }
       const int j = 2 * v, t = j >> 3;
@@ -630,10 +696,17 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     tc::tmem_ld16_nowait(tq + 64, zv[0]);
     tc::tmem_ld16_nowait(tq + 80, zv[1]);
     tc::tmem_wait_ld();
-    constexpr int KP = (KC + 1) & ~1;
+    // zT[u][8 kg + m] = z_{kg KH + m}[u] (precode_sw128_h), zero padded
+    constexpr int KH = (KC + 1) / 2;
     float4 *zo = reinterpret_cast<float4 *>(zT + l * FDT_SP);
+    auto sym = [](int pos) { return pos < 8 ? (pos < KH ? pos : -1) : (pos - 8 < KC - KH ? KH + pos - 8 : -1); };
 #pragma unroll
-    for (int j = 0; j < KP; j += 2) zo[j >> 1] = make_float4(zv[0][j], zv[1][j], zv[0][j + 1], zv[1][j + 1]);
+    for (int pos = 0; pos < 16; pos += 2) {
+      const int k0 = sym(pos), k1 = sym(pos + 1);
+      if (k0 < 0 && k1 < 0) continue;
+      zo[pos >> 1] = make_float4(k0 >= 0 ? zv[0][k0 & 15] : 0.f, k0 >= 0 ? zv[1][k0 & 15] : 0.f,
+                                 k1 >= 0 ? zv[0][k1 & 15] : 0.f, k1 >= 0 ? zv[1][k1 & 15] : 0.f);
+    }
     tc::fence_before_sync();
     named_sync(1, 128);                                       // TMEM reads done
     if (warp == 0) {
@@ -658,7 +731,10 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   }
   __syncwarp();
   if (active) {
-    float pw = (DP_FD_ABL & 2) ? 0.f : precode_sw128<KC>(tl, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S, (size_t)a.Bl, l, FDT_SP);
+    float2 *xo = a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S;
+    float pw = (DP_FD_ABL & 2) ? 0.f
+               : WTC ? precode_sw128_h<KC>(tl, zT, a.K, xo, (size_t)a.Bl, l)
+                     : precode_sw128<KC>(tl, zT, a.K, xo, (size_t)a.Bl, l, FDT_SP);
     pw = sg_sum<U>(pw);
     if (l == 0) {
       a.beta[pr] = ok ? beta : qnan();

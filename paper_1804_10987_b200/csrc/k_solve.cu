@@ -13,13 +13,15 @@ int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
   if constexpr (U == 32) {
     static const bool sg_only = getenv("DP_SOLVE_SG") != nullptr;   // A/B: one warp per problem
     static const int nw_env = getenv("DP_SOLVE_NW") ? atoi(getenv("DP_SOLVE_NW")) : 4;
+    static const bool blk = getenv("DP_SOLVE_BLK") && atoi(getenv("DP_SOLVE_BLK")) == 1;   // A/B: 1 = blocked sweep
     if (!sg_only) {                                                  // 4 (or 2) warps per problem (solve_mw.cuh)
       const int NW = nw_env == 2 ? 2 : 4;
       // whitening in symbol chunks of at most 8: at 9 CTAs / SM (56 registers) 14 or 16
       // accumulators spilled
       constexpr int KS = KC > 8 ? KC / 2 : KC;
       const size_t sm = (size_t)dpk::smw_smem_elems(a.K, KS, NW) * sizeof(float2);
-      auto kern = NW == 4 ? dpk::solve_mw_kernel<KS, 4> : dpk::solve_mw_kernel<KS, 2>;
+      auto kern = NW == 4 ? (blk ? dpk::solve_mw_kernel<KS, 4, true> : dpk::solve_mw_kernel<KS, 4, false>)
+                          : dpk::solve_mw_kernel<KS, 2>;
       CK(set_smem(kern, sm));
       LaunchScope ls(c, DP_KERNEL_SOLVE, st);
       CK(launch_pdl(kern, dim3((nprob + 4 / NW - 1) / (4 / NW)), dim3(dpk::SMW_THREADS), sm, st, a));
@@ -28,7 +30,9 @@ int launch_solve(dp_ctx *c, const Args &a, cudaStream_t st) {
   }
   // few problems (PD: one per subcarrier): one warp per CTA spreads the ~9k-instruction
   // warps evenly over the SMs (4-warp CTAs left some SMs with 50% more work)
-  const int wpc = (nprob / (32 / U) <= 16 * c->num_sms) ? 1 : 4;
+  static const int wpc_env = getenv("DP_SOLVE_WPC") ? atoi(getenv("DP_SOLVE_WPC")) : 0;   // A/B: warps per CTA
+  const int wpc = (wpc_env == 1 || wpc_env == 2 || wpc_env == 4) ? wpc_env
+                  : (nprob / (32 / U) <= 16 * c->num_sms) ? 1 : 4;
   const int per = wpc * (32 / U);
   const size_t sm = smem_solve(U, a.K) / 4 * wpc;
   auto kern = dpk::solve_kernel<U, KC>;

@@ -999,9 +999,12 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
   __syncwarp();
   float2 col[U];
   load_packed_col<U>(Gs, l, a.kappa, col);
-  bool ok;
+  bool ok = true;
   const float dl = Gs[pidx(U, l, l)].x + a.kappa;          // diagonal entry of this lane's column
-  const float beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
+#ifndef DP_SOLVE_ABL
+#define DP_SOLVE_ABL 0   // diagnostics builds only: 1 no sweep, 2 no whitening (timing ablation)
+#endif
+  const float beta = (DP_SOLVE_ABL & 1) ? 1.f : sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]
   const float ib = ok ? -__fdividef(1.f, beta) : 0.f;
   if (a.Wout) {                                   // prepare: cache W = A^{-1} / beta (upper, packed)
     if (active) {
@@ -1022,7 +1025,7 @@ __global__ void __launch_bounds__(128) solve_kernel(Args a) {
     transpose_s<U, KC>(ss, sT, a.K, l);
     __syncwarp();
     zT = ss;
-    whiten_Tg<U, KC>(col, ib, sT, zT, a.K, l);
+    if (!(DP_SOLVE_ABL & 2)) whiten_Tg<U, KC>(col, ib, sT, zT, a.K, l);
   } else {
     whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
   }
