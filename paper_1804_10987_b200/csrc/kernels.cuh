@@ -786,7 +786,7 @@ __device__ __forceinline__ void finish_sc(const Args &a, int sc) {
 // -> beta_c -> z = A^{-1} s / beta_c -> x_c = H_c^H z -> power partial.
 // smem per SG: tile S*U + scratch U + max(U/2 (U/2 + 2), K*U + U*zs).
 template <int U, int KC>
-__global__ void __launch_bounds__(128, 3) fd_fused_kernel(Args a) {
+__global__ void __launch_bounds__(128, U == 16 ? 4 : 3) fd_fused_kernel(Args a) {
   pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
                    // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
