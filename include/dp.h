@@ -41,7 +41,9 @@
  * Pointers may be DEVICE pointers (the fast path; the caller owns them, the
  * call is asynchronous on `stream`) or HOST pointers (pinned or pageable; the
  * library stages them through context-owned device buffers with H2D / D2H
- * copies on `stream` and the call returns after the D2H copy completed).
+ * copies on `stream` and the call returns after the D2H copy completed;
+ * with DP_FLAG_HOST_ASYNC at world == 1 it returns once the copies and kernels
+ * are enqueued, see the flag).
  * All of H_local, s, x_local must be of the same kind.  `stream` is a
  * cudaStream_t passed as void* (NULL = legacy default stream).
  * The context owns every workspace (sized at dp_init; precode calls perform
@@ -87,6 +89,16 @@ extern "C" {
 #define DP_FLAG_PROFILE     4  /* bracket every kernel launch with CUDA events (dp_profile_read)        */
 #define DP_FLAG_FORCE_COMM  8  /* world == 1: still issue the NCCL collectives (tests the comm path);
                                   requires nccl_id                                                     */
+#define DP_FLAG_HOST_ASYNC 32  /* host-pointer precode calls at world == 1 (the chunked H2D / kernels /
+                                  D2H pipeline) return once the work is enqueued: x (and the scalars)
+                                  are complete, and H, s, x may be reused by the host, only after
+                                  `stream` has been synchronized.  Consecutive calls of the context then
+                                  overlap: a call's H2D of chunk i waits only for the previous call's
+                                  kernels on chunk i (not for the whole previous call), its kernels on
+                                  chunk i for the previous D2H of chunk i; the H2D is not ordered after
+                                  other work the caller queued on `stream`.  Device-pointer calls and
+                                  world > 1 are unaffected.  A streaming mode for frame sequences
+                                  (a new channel and symbol block every frame)            */
 #define DP_FLAG_FP64       16  /* accuracy option (SURVEY.md §8(b) "DP_GRAM_FP64"): Gram,
                                   regularised solve, beta, whitening and precode accumulate in fp64
                                   (H, s, x stay complex64).  For square clusters (B_c = U) at high SNR

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DP_LIB_PATH") or os.path.join(_HERE, "libdp.so")   # override: A/B experiments
 
 DP_OK, DP_ERR_NUMERIC, DP_ERR_INVALID, DP_ERR_CUDA, DP_ERR_NCCL, DP_ERR_UNSUPPORTED = range(6)
-DP_FLAG_SYNC, DP_FLAG_UNFUSED, DP_FLAG_PROFILE, DP_FLAG_FORCE_COMM, DP_FLAG_FP64 = 1, 2, 4, 8, 16
+DP_FLAG_SYNC, DP_FLAG_UNFUSED, DP_FLAG_PROFILE, DP_FLAG_FORCE_COMM, DP_FLAG_FP64, DP_FLAG_HOST_ASYNC = 1, 2, 4, 8, 16, 32
 DP_PD_ALLREDUCE, DP_PD_REDUCE_BCAST, DP_PD_SCATTER_GATHER, DP_PD_NVLINK = 0, 1, 2, 3
 DP_SCALAR_BETA, DP_SCALAR_RX, DP_SCALAR_POWER = 0, 1, 2
 COMM_KINDS = ["gram", "s_bcast", "z_bcast", "scalars"]   # DP_COMM_* order

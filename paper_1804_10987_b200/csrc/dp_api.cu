@@ -490,7 +490,8 @@ int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c3
                    dp_c32 *x, cudaStream_t st) {
   const dp_config k = c->cfg;
   static const int nch_env = getenv("DP_HOST_CHUNKS") ? atoi(getenv("DP_HOST_CHUNKS")) : 8;
-  const int nch = std::max(1, std::min(nch_env, k.n_sc));
+  const int nch = std::max(1, std::min(std::min(nch_env, k.n_sc), (int)dp_ctx::HP_MAXCH));
+  const bool async = (k.flags & DP_FLAG_HOST_ASYNC) != 0;
   const size_t rowH = (size_t)c->Bl * k.U, rowS = (size_t)k.K * k.U, rowX = (size_t)k.K * c->Bl;
   if (!c->h_dev) {
     RET(alloc((void **)&c->h_dev, (size_t)k.n_sc * rowH * 8));
@@ -501,9 +502,15 @@ int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c3
     CK(cudaStreamCreateWithFlags(&c->st_h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st_d2h, cudaStreamNonBlocking));
   }
+  if (async && !c->hp_kdone[0])
+    for (int i = 0; i < dp_ctx::HP_MAXCH; ++i) {
+      CK(cudaEventCreateWithFlags(&c->hp_kdone[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->hp_d2h[i], cudaEventDisableTiming));
+    }
+  const bool chain = async && c->hp_nch == nch;            // previous async call with the same chunks
   cudaEvent_t ev_start = take_event(c);
   CK(cudaEventRecord(ev_start, st));                       // after the caller's prior work
-  CK(cudaStreamWaitEvent(c->st_h2d, ev_start, 0));
+  if (!chain) CK(cudaStreamWaitEvent(c->st_h2d, ev_start, 0));
   float *beta0 = c->beta, *fin0 = c->fin;
   int rc = DP_OK;
   std::vector<cudaEvent_t> evs;
@@ -513,10 +520,12 @@ int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c3
     cudaEvent_t ein = take_event(c), eout = take_event(c);
     evs.push_back(ein);
     evs.push_back(eout);
+    if (chain) CK(cudaStreamWaitEvent(c->st_h2d, c->hp_kdone[i], 0));   // staging chunk i free
     CK(cudaMemcpyAsync(c->h_dev + sc0 * rowH, H + sc0 * rowH, n * rowH * 8, cudaMemcpyHostToDevice, c->st_h2d));
     CK(cudaMemcpyAsync(c->s_dev + sc0 * rowS, s + sc0 * rowS, n * rowS * 8, cudaMemcpyHostToDevice, c->st_h2d));
     CK(cudaEventRecord(ein, c->st_h2d));
     CK(cudaStreamWaitEvent(st, ein, 0));
+    if (chain) CK(cudaStreamWaitEvent(st, c->hp_d2h[i], 0));   // x staging chunk i copied out
     c->cfg.n_sc = n;                                        // chunk view of the context
     c->beta = beta0 + (size_t)sc0 * groups;
     c->fin = fin0 + (size_t)sc0 * 2;
@@ -528,9 +537,19 @@ int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c3
     CK(cudaEventRecord(eout, st));
     CK(cudaStreamWaitEvent(c->st_d2h, eout, 0));
     CK(cudaMemcpyAsync(x + sc0 * rowX, c->x_dev + sc0 * rowX, n * rowX * 8, cudaMemcpyDeviceToHost, c->st_d2h));
+    if (async) {
+      CK(cudaEventRecord(c->hp_kdone[i], st));
+      CK(cudaEventRecord(c->hp_d2h[i], c->st_d2h));
+    }
   }
-  CK(cudaStreamSynchronize(c->st_d2h));
-  CK(cudaStreamSynchronize(st));
+  if (async) {                                             // syncing `stream` covers the last D2H
+    c->hp_nch = rc == DP_OK ? nch : 0;
+    if (rc == DP_OK) CK(cudaStreamWaitEvent(st, c->hp_d2h[nch - 1], 0));
+  } else {
+    c->hp_nch = 0;
+    CK(cudaStreamSynchronize(c->st_d2h));
+    CK(cudaStreamSynchronize(st));
+  }
   for (auto e : evs) c->ev_pool.push_back(e);
   c->ev_pool.push_back(ev_start);
   return rc;
@@ -879,6 +898,10 @@ int dp_finalize(dp_ctx *c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm && (c->lsa || c->devcomm || c->win_g || c->win_z || c->win_b)) lsa_teardown(c);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (int i = 0; i < dp_ctx::HP_MAXCH; ++i) {
+    if (c->hp_kdone[i]) cudaEventDestroy(c->hp_kdone[i]);
+    if (c->hp_d2h[i]) cudaEventDestroy(c->hp_d2h[i]);
+  }
   if (c->st_h2d) cudaStreamDestroy(c->st_h2d);
   if (c->st_d2h) cudaStreamDestroy(c->st_d2h);
   for (int j = 0; j < 3; ++j) {

@@ -87,6 +87,10 @@ struct dp_ctx {
   // host staging (host-pointer calls)
   float2 *h_dev = nullptr, *s_dev = nullptr, *x_dev = nullptr;
   cudaStream_t st_h2d = nullptr, st_d2h = nullptr;   // host-pointer pipeline copy streams
+  // DP_FLAG_HOST_ASYNC: per-chunk completion of the last call (kernels on chunk i, D2H of chunk i)
+  static constexpr int HP_MAXCH = 64;
+  cudaEvent_t hp_kdone[HP_MAXCH] = {}, hp_d2h[HP_MAXCH] = {};
+  int hp_nch = 0;                                    // chunks of the last async call (0: none pending)
   cudaStream_t st_side = nullptr;                    // side stream: s broadcast beside the PD Gram
   cudaEvent_t ev_side0 = nullptr, ev_side1 = nullptr;
   // host-side caches (per-frame host overhead): tensor maps by (pointer, rows, box, swizzle),

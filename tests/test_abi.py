@@ -43,6 +43,7 @@ def test_binding_constants_match_header():
     assert d["DP_ERR_NCCL"] == L.DP_ERR_NCCL and d["DP_ERR_UNSUPPORTED"] == L.DP_ERR_UNSUPPORTED
     assert d["DP_FLAG_SYNC"] == L.DP_FLAG_SYNC and d["DP_FLAG_UNFUSED"] == L.DP_FLAG_UNFUSED
     assert d["DP_FLAG_PROFILE"] == L.DP_FLAG_PROFILE and d["DP_FLAG_FORCE_COMM"] == L.DP_FLAG_FORCE_COMM
+    assert d["DP_FLAG_FP64"] == L.DP_FLAG_FP64 and d["DP_FLAG_HOST_ASYNC"] == L.DP_FLAG_HOST_ASYNC
     assert d["DP_PD_ALLREDUCE"] == L.DP_PD_ALLREDUCE and d["DP_PD_REDUCE_BCAST"] == L.DP_PD_REDUCE_BCAST
     assert d["DP_SCALAR_BETA"] == L.DP_SCALAR_BETA and d["DP_SCALAR_RX"] == L.DP_SCALAR_RX
     assert d["DP_SCALAR_POWER"] == L.DP_SCALAR_POWER

@@ -335,6 +335,39 @@ def test_host_pipeline_chunks_scalars(cfgid):
         assert np.array_equal(bh, bd) and np.array_equal(rxh, rxd) and np.array_equal(pwh, pwd), mode
 
 
+@pytest.mark.parametrize("cfgid", [3, 4])
+def test_host_async_consecutive_frames(cfgid):
+    """DP_FLAG_HOST_ASYNC (include/dp.h): host-pointer calls return once enqueued and consecutive
+    calls overlap (a call's H2D of chunk i waits only for the previous call's kernels on chunk i, its
+    kernels for the previous D2H of chunk i).  Five frames with distinct inputs, PD and FD
+    alternating, output buffers reused every other frame: after one stream synchronisation every
+    frame's x equals the synchronous call's bytes."""
+    cfg = CONFIGS[cfgid]
+    n_sc = 48
+    fs = [frame(cfg, n_sc, frame_id=10 + i) for i in range(5)]
+    modes = ["pd", "fd", "pd", "fd", "fd"]
+    with Precoder(n_sc, cfg.B, cfg.U, cfg.K, cfg.C, tau=cfg.tau) as pre:
+        ref = [(pre.precode_pd if m == "pd" else pre.precode_fd)(torch.from_numpy(f.H).pin_memory(),
+                                                                  torch.from_numpy(f.s).pin_memory(), 0.1, 1.0)
+               for f, m in zip(fs, modes)]
+    Hh = [torch.from_numpy(f.H).pin_memory() for f in fs]
+    Sh = [torch.from_numpy(f.s).pin_memory() for f in fs]
+    outs = [torch.empty_like(ref[0]).pin_memory() for _ in range(2)]
+    got = []
+    with Precoder(n_sc, cfg.B, cfg.U, cfg.K, cfg.C, tau=cfg.tau, flags=L.DP_FLAG_HOST_ASYNC) as pre:
+        for i, (m, _) in enumerate(zip(modes, fs)):
+            x = outs[i % 2]
+            (pre.precode_pd if m == "pd" else pre.precode_fd)(Hh[i], Sh[i], 0.1, 1.0, out=x)
+            if i % 2 == 1:                      # the two output buffers are complete after a sync
+                torch.cuda.synchronize()
+                got += [outs[0].clone(), outs[1].clone()]
+        torch.cuda.synchronize()
+        got.append(outs[0].clone())
+        assert pre.status() == 0
+    for i in range(5):
+        assert np.array_equal(got[i].numpy(), ref[i].numpy()), (i, modes[i])
+
+
 @pytest.mark.parametrize("Bl", [32, 64, 128])
 @pytest.mark.parametrize("mode", ["pd", "fd"])
 def test_u32_per_rank_shapes(Bl, mode):
