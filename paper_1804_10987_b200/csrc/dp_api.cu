@@ -511,6 +511,8 @@ int host_pipelined(dp_ctx *c, DevFn fn, int groups, const dp_c32 *H, const dp_c3
   cudaEvent_t ev_start = take_event(c);
   CK(cudaEventRecord(ev_start, st));                       // after the caller's prior work
   if (!chain) CK(cudaStreamWaitEvent(c->st_h2d, ev_start, 0));
+  else CK(cudaStreamWaitEvent(st, c->hp_kdone[nch - 1], 0));   // the workspace: previous call's kernels done
+                                                                // (a no-op when both calls use one stream)
   float *beta0 = c->beta, *fin0 = c->fin;
   int rc = DP_OK;
   std::vector<cudaEvent_t> evs;
