@@ -335,6 +335,45 @@ def test_host_pipeline_chunks_scalars(cfgid):
         assert np.array_equal(bh, bd) and np.array_equal(rxh, rxd) and np.array_equal(pwh, pwd), mode
 
 
+_VARIANT_SCRIPT = r"""
+import json, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import oracle
+from paper_1804_10987_b200 import CONFIGS, synth
+from paper_1804_10987_b200.api import Precoder
+from helpers import rel_l2
+cfg = CONFIGS[4]
+f = synth.make_frame(cfg.cfg_id, 29, cfg.B, cfg.U, cfg.K, cfg.M, frame=3)
+N0 = synth.n0_from_snr_db(cfg.snr_db)
+with Precoder(29, cfg.B, cfg.U, cfg.K, cfg.C) as pre:
+    x = pre.precode_pd(torch.from_numpy(f.H).cuda(), torch.from_numpy(f.s).cuda(), N0, 1.0)
+    beta = pre.read_scalars("beta").cpu().numpy()
+    torch.cuda.synchronize()
+    nbad = pre.status()
+xr, br = oracle.pd(f.H, f.s, cfg.C, N0, 1.0)
+print(json.dumps({"rel": rel_l2(x.cpu().numpy(), xr), "beta": float(np.max(np.abs(beta.reshape(br.shape) / br - 1))),
+                  "nbad": int(nbad)}))
+"""
+
+
+@pytest.mark.parametrize("env", [{"DP_SOLVE_BLK": "1"}, {"DP_SOLVE_SG": "1", "DP_SOLVE_WPC": "4"},
+                                 {"DP_SOLVE_NW": "2"}], ids=["blocked", "one_warp_wpc4", "two_warp"])
+def test_pd_solve_variants(env):
+    """The A/B variants of the PD solve (switches read once per process, so each runs in a child
+    process): the blocked 4-warp sweep, the one-warp solve in 4-warp CTAs, the two-warp row split --
+    cfg4 PD frame vs the oracle at the 1e-4 bar."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["nbad"] == 0 and out["rel"] <= REL_TOL and out["beta"] <= REL_TOL, out
+
+
 @pytest.mark.parametrize("cfgid", [3, 4])
 def test_host_async_consecutive_frames(cfgid):
     """DP_FLAG_HOST_ASYNC (include/dp.h): host-pointer calls return once enqueued and consecutive
