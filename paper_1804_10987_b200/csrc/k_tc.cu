@@ -89,14 +89,19 @@ bool fd_tc_ok(const dp_ctx *c, const Args &a) {
   return !off && c->use_tc && c->cfg.U == 32 && a.S == 32 && a.K <= 16;
 }
 
-// fd_tc folds the per-subcarrier scalars into the kernel (no fd_finish_kernel) when the
-// rank's clusters of a subcarrier fill whole CTAs (Cl = 4, 8, 16, 32: a cluster of Cl/4
-// CTAs) or a CTA holds whole subcarriers (Cl = 1, 2, 4).  Returns CTAs per subcarrier, 0 = off.
+// fd_tc folds the per-subcarrier scalars into the kernel (no fd_finish_kernel) when a CTA holds
+// whole subcarriers (Cl = 1, 2, 4); with DP_FD_CLUSTER_FOLD also when the rank's clusters of a
+// subcarrier fill a thread-block cluster of Cl/4 CTAs (Cl = 8, 16, 32).  Returns CTAs per
+// subcarrier, 0 = off (fd_finish_kernel after the FD kernel).
 int fd_fold_of(const dp_ctx *c, const Args &a) {
   static const bool off = getenv("DP_NO_FOLD") != nullptr;
+  static const bool cl_fold = getenv("DP_FD_CLUSTER_FOLD") != nullptr;   // A/B: thread-block-cluster fold
   if (off || a.Gout || !c->vruns.empty()) return 0;
   const int Cl = a.nchunks;
-  if (Cl == 4 || Cl == 8 || Cl == 16 || Cl == 32) return Cl / 4;
+  if (Cl == 4) return 1;                                   // one CTA = one subcarrier: in-CTA fold
+  // Cl = 8, 16, 32: a CTA cluster of Cl/4 waits for its slowest CTA before the sums (cfg4: FD kernel
+  // 137.8 us with the 2-CTA cluster fold, 133.8 us without + fd_finish_kernel); opt-in
+  if (cl_fold && (Cl == 8 || Cl == 16 || Cl == 32)) return Cl / 4;
   if (4 % Cl == 0) return 1;
   return 0;
 }

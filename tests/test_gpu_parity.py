@@ -729,7 +729,8 @@ def test_consecutive_frames_cfg4():
     back to back (PDL lets each kernel start while its predecessor drains, so mbarrier-phase or
     hand-off hazards that a single synchronised frame hides show up here), 600 subcarriers so the
     persistent PD kernels loop over several items per CTA; every frame against the oracle, and
-    the FD scalars folded into the tensor-core kernel (no finish kernel)."""
+    the FD scalars summed by one fd_finish_kernel per FD frame (the 2-CTA cluster fold is the opt-in
+    DP_FD_CLUSTER_FOLD variant, test_fd_cluster_fold_variant)."""
     cfg = CONFIGS[4]
     n_sc = 600
     f = frame(cfg, n_sc)
@@ -750,8 +751,56 @@ def test_consecutive_frames_cfg4():
             assert np.max(np.abs(pw / pwr - 1)) <= 1e-4
         p = pre.profile(reset=True)
         assert pre.status() == 0
-    assert p["fused_fd"]["launches"] == 3 and p["finish"]["launches"] == 0
+    assert p["fused_fd"]["launches"] == 3 and p["finish"]["launches"] == 3
     assert p["solve"]["launches"] == 2 and p["precode"]["launches"] == 2
+
+
+_FOLD_SCRIPT = r"""
+import json, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import oracle
+from paper_1804_10987_b200 import CONFIGS, synth
+from paper_1804_10987_b200 import _lib as L
+from paper_1804_10987_b200.api import Precoder
+from helpers import rel_l2
+cfg = CONFIGS[4]
+f = synth.make_frame(cfg.cfg_id, 40, cfg.B, cfg.U, cfg.K, cfg.M, frame=5)
+N0 = synth.n0_from_snr_db(cfg.snr_db)
+out = {}
+with Precoder(40, cfg.B, cfg.U, cfg.K, cfg.C, tau=cfg.tau, flags=L.DP_FLAG_PROFILE) as pre:
+    H, s = torch.from_numpy(f.H).cuda(), torch.from_numpy(f.s).cuda()
+    for i in range(3):                                   # back-to-back frames
+        x = pre.precode_fd(H, s, N0, 1.0)
+    beta = pre.read_scalars("beta").cpu().numpy()
+    rx = pre.read_scalars("rx").cpu().numpy()
+    torch.cuda.synchronize()
+    out["nbad"] = int(pre.status())
+    p = pre.profile(reset=True)
+    out["finish"] = p["finish"]["launches"]
+xr, br = oracle.fd(f.H, f.s, cfg.C, N0, 1.0, tau=cfg.tau)
+rxr = oracle.rx_scale_fd(br)
+out["rel"] = rel_l2(x.cpu().numpy(), xr)
+out["beta"] = float(np.max(np.abs(beta.reshape(br.shape) / br - 1)))
+out["rx"] = float(np.max(np.abs(rx / rxr - 1)))
+print(json.dumps(out))
+"""
+
+
+def test_fd_cluster_fold_variant():
+    """DP_FD_CLUSTER_FOLD=1 (k_tc.cu, read once per process, so in a child process): the cfg4 FD
+    scalars summed in-kernel across a 2-CTA thread-block cluster (st.async into rank 0's shared
+    memory) instead of fd_finish_kernel -- no finish launch, x / beta / rx vs the oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FOLD_SCRIPT, root], env={**os.environ, "DP_FD_CLUSTER_FOLD": "1"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["finish"] == 0 and out["nbad"] == 0, out
+    assert out["rel"] <= REL_TOL and out["beta"] <= REL_TOL and out["rx"] <= REL_TOL, out
 
 
 @pytest.mark.parametrize("unfused", [False, True], ids=["single-pass", "unfused"])
