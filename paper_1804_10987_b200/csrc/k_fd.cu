@@ -65,7 +65,13 @@ int launch_mrt_u(dp_ctx *c, const Args &a, cudaStream_t st) {
 
 int launch_fd_finish(dp_ctx *c, const Args &a, cudaStream_t st) {
   LaunchScope ls(c, DP_KERNEL_FINISH, st);
-  CK(launch_pdl(dpk::fd_finish_kernel, dim3((a.n_sc + 127) / 128), dim3(128), 0, st, a));
+  Args b = a;                                              // b.rep = lanes per subcarrier (fd_finish_kernel)
+  const int mx = std::max(a.nbeta, a.nchunks);
+  b.rep = 1;
+  while (b.rep < mx) b.rep *= 2;
+  if (b.rep > 32) b.rep = 0;                               // many small clusters: thread per subcarrier
+  const long long nt = (long long)a.n_sc * (b.rep ? b.rep : 1);
+  CK(launch_pdl(dpk::fd_finish_kernel, dim3((unsigned)((nt + 127) / 128)), dim3(128), 0, st, b));
   return DP_OK;
 }
 

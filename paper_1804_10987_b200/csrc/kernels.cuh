@@ -1174,35 +1174,31 @@ __global__ void __launch_bounds__(128) mrt_kernel(Args a) {
 // Per subcarrier, fixed order over the local clusters: fin[sc] = {sum_c 1/beta_c,
 // sum_c power_c}.  (A separate grid: folding it into the fused kernel needs a
 // release fence per cluster, which waits for that warp's x stores and cost ~10%.)
-// All of a subcarrier's partials are loaded before the sums (up to 32 per kind in flight instead of a
-// dependent load per term: 8.6 -> ~1 us at cfg4); the sums run in finish_sc's order (ascending
-// cluster), so the scalars are bit-identical to finish_sc's and to the in-kernel folds'.
+// G = a power of two >= the rank's clusters lanes per subcarrier (a.rep reused as G, set by the
+// launcher): lane c loads cluster c's beta and power partial (coalesced, one load per lane instead of a
+// dependent load per term), lane 0 of the group sums them in ascending cluster order through
+// shuffles -- the order of finish_sc, so the scalars are bit-identical to it and to the in-kernel folds.
 static __global__ void __launch_bounds__(128) fd_finish_kernel(Args a) {
   pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
                    // (it still waits for this grid's completion in griddepcontrol.wait)
   pdl_wait();
-  const int sc = blockIdx.x * blockDim.x + threadIdx.x;
-  if (sc >= a.n_sc) return;
-  constexpr int MAXP = 32;
-  if (a.nbeta > MAXP || a.nchunks > MAXP) {
-    finish_sc(a, sc);
+  if (a.rep == 0) {                                        // > 32 partials: one thread per subcarrier
+    const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sc < a.n_sc) finish_sc(a, sc);
     return;
   }
-  float vb[MAXP], vp[MAXP];
-#pragma unroll
-  for (int c = 0; c < MAXP; ++c) {
-    vb[c] = c < a.nbeta ? __ldcg(a.beta + (size_t)sc * a.nbeta + c) : 1.f;
-    vp[c] = c < a.nchunks ? __ldcg(a.pw + (size_t)sc * a.nchunks + c) : 0.f;
-  }
+  const int G = a.rep, t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int sc = t / G, c = t % G, lane = threadIdx.x & 31, base = lane - c;
+  const bool in = sc < a.n_sc;
+  const float vb = (in && c < a.nbeta) ? 1.f / __ldcg(a.beta + (size_t)sc * a.nbeta + c) : 0.f;
+  const float vp = (in && c < a.nchunks) ? __ldcg(a.pw + (size_t)sc * a.nchunks + c) : 0.f;
   float ib = 0.f, p = 0.f;
-#pragma unroll
-  for (int c = 0; c < MAXP; ++c)
-    if (c < a.nbeta) ib += 1.f / vb[c];
-#pragma unroll
-  for (int c = 0; c < MAXP; ++c)
-    if (c < a.nchunks) p += vp[c];
-  a.fin[2 * sc] = a.fin_inv_beta ? ib : 0.f;
-  a.fin[2 * sc + 1] = p;
+  for (int j = 0; j < a.nbeta; ++j) ib += __shfl_sync(0xffffffffu, vb, base + j);
+  for (int j = 0; j < a.nchunks; ++j) p += __shfl_sync(0xffffffffu, vp, base + j);
+  if (in && c == 0) {
+    a.fin[2 * sc] = a.fin_inv_beta ? ib : 0.f;
+    a.fin[2 * sc + 1] = p;
+  }
 }
 
 // ================================================================== FD finish, unequal clusters
