@@ -33,8 +33,8 @@ __host__ __device__ inline int fds_size(int K) {
 template <int S, int U, int KC>
 __global__ void __launch_bounds__(128) fd_small_kernel(Args a) {
   pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
-                   // (it still waits for this grid's completion in griddepcontrol.wait)
-  pdl_wait();
+                   // (it still waits for this grid's completion in griddepcontrol.wait; this kernel's
+                   // own wait sits before its first output write, see below)
   constexpr int PPW = 32 / S;
   extern __shared__ __align__(16) float2 smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(128) fd_small_kernel(Args a) {
   __syncwarp();
   whiten_sg<S, KC>(col, ib, t, K, 0, 1, zT, l);                          // zT[l][k] = x_k[l]
   __syncwarp();
+  pdl_wait();   // H, s are inputs of the call; nothing above touches a predecessor's outputs
   float pw = 0.f;
   if (active && real) {
     const int zs = ZL<KC>::zs(K);

@@ -444,7 +444,10 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tm = tmem_base;
-  pdl_wait();
+  // Programmatic dependent launch: nothing before the x stores reads or writes an output of a
+  // preceding kernel (H and s are inputs of the call; the Gram, sweep and whitening live in this
+  // CTA's shared memory and TMEM), so griddepcontrol.wait sits just before them -- CTAs that start
+  // on SMs the preceding kernel has already left run their problems up to the precode meanwhile.
 
   // ---------------------------------------------------------------- solver warps 0-3
   const int p = warp;
@@ -535,6 +538,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
   }
   const int pr = p0 + p;
   float fold_b = 0.f, fold_p = 0.f;                           // this problem's 1/beta_c and power (fold)
+  if (a.Gout) pdl_wait();
   if (active && a.Gout) {                                     // dp_debug_gram: packed G_c of the FD path
     const float2 *g = reinterpret_cast<const float2 *>(rg) + lane * FDT_GLD;
     for (int u = 0; u <= lane; ++u) a.Gout[(size_t)pr * npacked(32) + pidx(32, u, lane)] = g[u];
@@ -730,6 +734,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
     }
   }
   __syncwarp();
+  pdl_wait();                                                 // the predecessor's outputs (x, beta, ...) complete
   if (active) {
     float2 *xo = a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S;
     float pw = (DP_FD_ABL & 2) ? 0.f

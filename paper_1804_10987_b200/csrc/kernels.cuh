@@ -788,8 +788,8 @@ __device__ __forceinline__ void finish_sc(const Args &a, int sc) {
 template <int U, int KC>
 __global__ void __launch_bounds__(128, U == 16 ? 4 : 3) fd_fused_kernel(Args a) {
   pdl_trigger();   // early: the next kernel may launch once every CTA of this grid has started
-                   // (it still waits for this grid's completion in griddepcontrol.wait)
-  pdl_wait();
+                   // (it still waits for this grid's completion in griddepcontrol.wait; this kernel's
+                   // own wait sits before its first output write, see below)
   constexpr int PPW = 32 / U;
   extern __shared__ __align__(16) float2 smem[];
   const int nw = blockDim.x >> 5;
@@ -876,6 +876,7 @@ __global__ void __launch_bounds__(128, U == 16 ? 4 : 3) fd_fused_kernel(Args a) 
     whiten_sg<U, KC>(col, ib, ss, a.K, 0, 1, zT, l);
   }
   __syncwarp();
+  pdl_wait();   // H, s are inputs of the call; nothing above touches a predecessor's outputs
   float pw = 0.f;
   if (active)
     pw = precode_sg<U, KC>(tile, 0, a.S, zT, a.K, a.x + (size_t)sc * a.K * a.Bl + (size_t)cl * a.S,
