@@ -212,6 +212,7 @@ int fd_var_runs(dp_ctx *c, const float2 *Hd, const float2 *s_use, double N0, dou
     a.H = Hd + (size_t)r.off * k.U;
     a.hrow_off = r.off;
     a.s = s_use;
+    a.s_wait = c->comm_on && !k.s_on_all_ranks;
     a.x = xd + r.off;
     a.S = r.S;
     a.nchunks = r.len;
@@ -250,6 +251,7 @@ int precode_fd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   Args a = base_args(c);
   a.H = Hd;
   a.s = s_use;
+  a.s_wait = c->comm_on && !k.s_on_all_ranks;             // s landed by ncclBroadcast on this stream
   a.x = xd;
   a.S = c->S;
   a.nchunks = c->Cl;

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(128) fd_small_kernel(Args a) {
     float4 *dst = reinterpret_cast<float4 *>(Hs + l * U);
 #pragma unroll
     for (int c = 0; c < U / 2; ++c) dst[c] = real ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.s_wait) pdl_wait();                                 // s from the broadcast: its kernel complete
     for (int i = l; i < K * U / 2; i += S)
       reinterpret_cast<float4 *>(ss)[i] = reinterpret_cast<const float4 *>(a.s + (size_t)sc * K * U)[i];
   }

@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
       }
       __syncwarp();
       // s of this subcarrier -> warp 0's region (free until zT): read by the S' build after the sweep
+      if (a.s_wait) pdl_wait();                               // s from the broadcast: its kernel complete
       if (warp == 0) sg_copy_async<U>(reinterpret_cast<float2 *>(rg), a.s + (size_t)sc * a.K * U, a.K * U, l);
       beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);
 #else
@@ -645,6 +646,7 @@ __global__ void __launch_bounds__(FDT_THREADS, 3) fd_tc_kernel(const __grid_cons
       }
     }
     __syncwarp();
+    if (a.s_wait) pdl_wait();
     sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
     if (DP_FD_ABL & 1) ok = true;
     else if (active) beta = sweep_sg2<U>(col, slot, l, dl, a.kappa, a.coef, ok);   // col <- -A^{-1}[:, l]

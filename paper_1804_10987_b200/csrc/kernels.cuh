@@ -755,6 +755,8 @@ struct Args {
   int fold;             // fd_tc: per-subcarrier scalars in-kernel (CTAs per subcarrier; 0 = finish kernel)
   int hrow_off;         // host only: H rows before a.H in its allocation (unequal-cluster runs; TMA extent)
   int rep;              // fd_fused: sub-groups per problem (1, 2, 4, 8; 0 = 1), see fd_fused_kernel
+  int s_wait;           // single-pass FD kernels: s was written by a collective / kernel earlier on the
+                        // stream (the s broadcast), so griddepcontrol.wait before reading it
   double kappa64, coef64;   // DP_FLAG_FP64 kernels (f64.cuh): kappa and coef unrounded
 };
 
@@ -854,6 +856,7 @@ __global__ void __launch_bounds__(128, U == 16 ? 4 : 3) fd_fused_kernel(Args a) 
     gacc_to_column<U>(g, T, l, a.kappa, col);
   }
   // stage s_k of this subcarrier into the (now free) T region while the sweep runs
+  if (a.s_wait) pdl_wait();
   sg_copy_async<U>(ss, a.s + (size_t)sc * a.K * U, a.K * U, l);
   bool ok;
   float dl = 0.f;                                         // this lane's diagonal entry A[l][l]
