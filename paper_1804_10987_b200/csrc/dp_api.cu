@@ -345,6 +345,7 @@ int precode_pd_dev(dp_ctx *c, const float2 *Hd, const float2 *sd, double N0, dou
   Args a = base_args(c);
   a.H = Hd;
   a.x = xd;
+  a.s_wait = c->comm_on;                                   // s may come from a collective on the stream
   a.S = c->pd_chunk;
   a.nchunks = c->pd_nchunks;
   set_params(a, (k.U * N0 / rho2), (k.Es / rho2));

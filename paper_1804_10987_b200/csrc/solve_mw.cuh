@@ -305,9 +305,14 @@ __global__ void __launch_bounds__(SMW_THREADS, NW == 4 ? 9 : 5) solve_mw_kernel(
     else asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NW * 32) : "memory");
   };
   if (pt == 0) bad = 0;
+  // s is an input of the call (unless a collective on the stream produced it: a.s_wait), so it is
+  // fetched before griddepcontrol.wait; G is the Gram kernel's output, fetched after it
+  const bool s_early = !a.Wout && !a.s_wait;            // prepare calls have no symbols
+  if (s_early)
+    for (int i = pt; i < a.K * U / 2; i += NW * 32) cp_async16(ss + 2 * i, a.s + (size_t)sc * a.K * U + 2 * i);
   pdl_wait();
   for (int i = pt; i < NP / 2; i += NW * 32) cp_async16(Gs + 2 * i, a.G + (size_t)p * NP + 2 * i);
-  if (!a.Wout)                                          // prepare calls have no symbols
+  if (!a.Wout && !s_early)
     for (int i = pt; i < a.K * U / 2; i += NW * 32) cp_async16(ss + 2 * i, a.s + (size_t)sc * a.K * U + 2 * i);
   cp_async_wait_all();
   psync();
