@@ -619,6 +619,29 @@ def main():
         p50 = xs[len(xs) // 2]
         lat[m] = {"latency_ms_p50": p50, "latency_ms_p99": xs[min(len(xs) - 1, int(0.99 * len(xs)))],
                   "frames": len(xs), "gbps_at_p50": bits_frame / (p50 / 1e3) / 1e9}
+        # steady state of this precoder alone: back-to-back frames (rotating resident inputs) captured
+        # into one CUDA graph and replayed, so consecutive frames overlap under PDL as in the step
+        if len(modes) > 1 and not args.eager:
+            nf = max(20, min(args.steps, 200))
+            try:
+                g1 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g1):
+                    for i in range(nf):
+                        j = i % R
+                        fn(Hs[j], Ss[j], N0, 1.0, out=Xs[j])
+                g1.replay()
+                barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g1.replay()
+                b.record(stream)
+                barrier()
+                sms = D.max_over_ranks(a.elapsed_time(b), dev) / nf
+                lat[m].update({"steady_ms_per_frame": sms, "steady_frames": nf,
+                               "gbps_steady": bits_frame / (sms / 1e3) / 1e9})
+                del g1
+            except Exception as e:                       # pragma: no cover - report, keep the line
+                lat[m]["steady_error"] = str(e)[:120]
     pre.profile(reset=True)
 
     # ---------------- prepare / apply: W = A^{-1}/beta cached once per
