@@ -117,7 +117,8 @@ int launch_fd_tc(dp_ctx *c, const Args &a, cudaStream_t st) {
   const int nprob = a.n_sc * a.nchunks;
   Args b = a;
   // resident CTAs: 3 per SM; the L2 prefetch assumes contiguous clusters (off for unequal runs)
-  b.pf_dist = a.Bl == a.nchunks * 32 ? 3 * c->num_sms : 0;
+  static const int pf_waves = getenv("DP_FD_PF") ? atoi(getenv("DP_FD_PF")) : 3;   // A/B: CTAs ahead / num_sms
+  b.pf_dist = a.Bl == a.nchunks * 32 ? pf_waves * c->num_sms : 0;
   b.fold = fd_fold_of(c, a);
   LaunchScope ls(c, DP_KERNEL_FUSED_FD, st);
   if (b.fold > 1)
